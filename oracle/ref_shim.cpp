@@ -1,0 +1,531 @@
+// oracle/ref_shim.cpp — TEST INFRASTRUCTURE ONLY (never part of the product).
+//
+// Exposes the UNMODIFIED reference implementation (compiled from the sources
+// under /root/reference/proj by oracle/Makefile into oracle/_ref/) through the
+// same C ABI as the product (include/e2sched.h), so tests and bench.py's
+// reference arm can drive both with identical calls.  Only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+// load it.
+//
+// Reference entry points wrapped (proj/include/kvsched/global_scheduler.hpp):
+//   ctor :101, schedule_request :104, decide :105, note_* :108-111,
+//   decode_ratio :113, gpu_load_ms :114, snapshot :115, prune_dead_nodes :119,
+//   mirror :121, redirects :122, stats :123; load_cost (cost_model.hpp:87-89);
+//   generate / assign_poisson_arrivals (workload.hpp:80,109).
+#include <algorithm>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "e2sched.h"
+#include "kvsched/cost_model.hpp"
+#include "kvsched/global_scheduler.hpp"
+#include "kvsched/prefix_tree.hpp"
+#include "kvsched/workload.hpp"
+
+using namespace kvsched;
+
+struct e2_handle {
+  std::unique_ptr<GlobalScheduler> s;
+  int n = 0;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+SchedulerConfig to_cfg(const e2_sched_cfg* c) {
+  SchedulerConfig s;
+  s.history_window_ms = c->history_window_ms;
+  s.th_bal = c->th_bal;
+  s.imbal_ratio = c->imbal_ratio;
+  s.priority_groups = static_cast<int>(c->priority_groups);
+  s.kv_capacity_tokens = c->kv_capacity_tokens;
+  s.default_output_len = c->default_output_len;
+  return s;
+}
+
+TimeModel to_model(const e2_time_model* m) {
+  TimeModel t;
+  t.prefill_base_ms = m->prefill_base_ms;
+  t.prefill_per_token_ms = m->prefill_per_token_ms;
+  t.decode_per_token_ms = m->decode_per_token_ms;
+  t.iteration_base_ms = m->iteration_base_ms;
+  return t;
+}
+
+GlobalPolicy to_policy(const e2_policy* p) {
+  GlobalPolicy g;
+  g.mode = p->mode == E2_MODE_ROUND_ROBIN ? GlobalMode::RoundRobin : GlobalMode::PrefixAware;
+  g.rebalance = p->rebalance != 0;
+  g.autoscale = p->autoscale != 0;
+  g.pd_balance = p->pd_balance != 0;
+  return g;
+}
+
+int32_t branch_code(Branch b) {
+  switch (b) {
+    case Branch::Exploit: return E2_BRANCH_EXPLOIT;
+    case Branch::Explore: return E2_BRANCH_EXPLORE;
+    case Branch::ExploreDecodePressure: return E2_BRANCH_DECODE_PRESSURE;
+    case Branch::RoundRobin: return E2_BRANCH_ROUND_ROBIN;
+  }
+  return -1;
+}
+
+void fill_cost(e2_cost* o, GpuId g, const CostBreakdown& c) {
+  o->gpu = g;
+  o->eviction_infeasible = c.eviction_infeasible ? 1 : 0;
+  o->current_load_ms = c.current_load_ms;
+  o->eviction_ms = c.eviction_ms;
+  o->prefill_ms = c.prefill_ms;
+}
+
+void fill_decision(const Decision& d, int64_t matched, int n, e2_decision* out, e2_cost* costs,
+                   double* ratios) {
+  if (out) {
+    out->request = d.request;
+    out->branch = branch_code(d.branch);
+    out->gpu = d.gpu;
+    out->redirected = d.redirected ? 1 : 0;
+    out->pre_redirect_gpu = d.pre_redirect_gpu;
+    out->n_costs = static_cast<int32_t>(d.costs.size());
+    out->has_ratios = d.decode_ratios.empty() ? 0 : 1;
+    out->cached_len = d.cached_len;
+    out->missed_len = d.missed_len;
+    out->missed_on_chosen = d.missed_on_chosen;
+    out->matched_len = matched;
+  }
+  if (costs) {
+    for (size_t i = 0; i < d.costs.size() && i < static_cast<size_t>(n + 1); ++i) {
+      fill_cost(&costs[i], d.costs[i].gpu, d.costs[i].cost);
+    }
+  }
+  if (ratios && !d.decode_ratios.empty()) {
+    for (int g = 0; g < n; ++g) {
+      auto it = d.decode_ratios.find(g);
+      ratios[g] = it == d.decode_ratios.end() ? 0.0 : it->second;
+    }
+  }
+}
+
+template <typename F>
+int guard(e2_handle* h, F&& f) {
+  try {
+    f();
+    return E2_OK;
+  } catch (const NoAdmissibleGpu& e) {
+    h->err = e.what();
+    return E2_ERR_NO_ADMISSIBLE;
+  } catch (const SimError& e) {
+    h->err = e.what();
+    return E2_ERR_SIM;
+  } catch (const ConfigError& e) {
+    h->err = e.what();
+    return E2_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return E2_ERR_ARG;
+  }
+}
+
+bool bad_gpu(e2_handle* h, int32_t g) {
+  if (g < 0 || g >= h->n) {
+    h->err = "gpu id out of range";
+    return true;
+  }
+  return false;
+}
+
+LoadWindow window_of(GlobalScheduler& s, int32_t g, double now) {
+  ClusterSnapshot snap = s.snapshot(now);
+  LoadWindow w(s.config().history_window_ms, s.config().default_output_len);
+  for (const auto& e : snap.gpus[g].scheduled) w.add_scheduled(e.t, e.missed, e.est_output);
+  for (const auto& c : snap.gpus[g].completed) w.add_completion(c.t, c.output);
+  return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* e2_backend(void) { return "reference"; }
+
+int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* model,
+              const e2_policy* policy, e2_handle** out) {
+  *out = nullptr;
+  try {
+    auto h = std::make_unique<e2_handle>();
+    h->s = std::make_unique<GlobalScheduler>(n_gpus, to_cfg(cfg), to_model(model),
+                                             to_policy(policy));
+    h->n = n_gpus;
+    *out = h.release();
+    return E2_OK;
+  } catch (const ConfigError& e) {
+    g_create_err = e.what();
+    return E2_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return E2_ERR_ARG;
+  }
+}
+
+void e2_destroy(e2_handle* h) { delete h; }
+
+const char* e2_last_error(const e2_handle* h) {
+  return h ? h->err.c_str() : g_create_err.c_str();
+}
+
+int e2_schedule(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t request_id,
+                double arrival_ms, double now, e2_decision* out, e2_cost* costs, double* ratios) {
+  return guard(h, [&] {
+    Request r;
+    r.id = request_id;
+    r.arrival_ms = arrival_ms;
+    r.prompt.assign(prompt, prompt + prompt_len);
+    const int64_t matched = h->s->mirror().match(r.prompt).matched_len;
+    Decision d = h->s->schedule_request(r, now);
+    fill_decision(d, matched, h->n, out, costs, ratios);
+  });
+}
+
+int e2_decide(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t request_id,
+              double now, e2_decision* out, e2_cost* costs, double* ratios) {
+  return guard(h, [&] {
+    Request r;
+    r.id = request_id;
+    r.prompt.assign(prompt, prompt + prompt_len);
+    const int64_t matched = h->s->mirror().match(r.prompt).matched_len;
+    Decision d = h->s->decide(r, now);
+    fill_decision(d, matched, h->n, out, costs, ratios);
+  });
+}
+
+int e2_note_admitted(e2_handle* h, int64_t request_id, double now) {
+  return guard(h, [&] { h->s->note_admitted(request_id, now); });
+}
+
+int e2_note_prefill_cached(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int32_t gpu,
+                           double now) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    TokenSeq p(prompt, prompt + prompt_len);
+    h->s->note_prefill_cached(p, gpu, now);
+  });
+}
+
+int e2_note_eviction(e2_handle* h, const int32_t* seq, int64_t seq_len, int64_t tail_len,
+                     int32_t gpu, double now) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    EvictedRange r;
+    r.seq.assign(seq, seq + seq_len);
+    r.tail_len = tail_len;
+    h->s->note_eviction(r, gpu, now);
+  });
+}
+
+int e2_note_finished(e2_handle* h, int64_t request_id, double now, int64_t output_len) {
+  return guard(h, [&] { h->s->note_finished(request_id, now, output_len); });
+}
+
+int e2_decode_ratio(e2_handle* h, int32_t gpu, double* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] { *out = h->s->decode_ratio(gpu); });
+}
+
+int e2_gpu_load_ms(e2_handle* h, int32_t gpu, double now, double* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] { *out = h->s->gpu_load_ms(gpu, now); });
+}
+
+int e2_prune_dead_nodes(e2_handle* h, double now, int64_t* removed) {
+  return guard(h, [&] { *removed = h->s->prune_dead_nodes(now); });
+}
+
+int e2_cached_tokens(e2_handle* h, int32_t gpu, int64_t* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] { *out = h->s->mirror().cached_tokens(gpu); });
+}
+
+int e2_node_count(e2_handle* h, int64_t* out) {
+  return guard(h, [&] { *out = h->s->mirror().node_count(); });
+}
+
+int e2_redirects(e2_handle* h, int32_t* out) {
+  return guard(h, [&] {
+    for (int g = 0; g < h->n; ++g) out[g] = -1;
+    for (auto& [s, t] : h->s->redirects()) out[s] = t;
+  });
+}
+
+int e2_get_stats(e2_handle* h, e2_stats* out) {
+  return guard(h, [&] {
+    const GlobalStats& s = h->s->stats();
+    out->exploit = s.exploit;
+    out->explore = s.explore;
+    out->decode_pressure = s.decode_pressure;
+    out->round_robin = s.round_robin;
+    out->redirected = s.redirected;
+    out->rebalance_installs = s.rebalance_installs;
+    out->autoscale_events = s.autoscale_events;
+    out->tree_reads = s.tree_reads;
+  });
+}
+
+int e2_load_cost(e2_handle* h, int32_t gpu, int64_t missed_tokens, double now, e2_cost* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    LoadWindow w = window_of(*h->s, gpu, now);
+    CostBreakdown c = load_cost(h->s->mirror(), w, gpu, h->s->config().kv_capacity_tokens,
+                                missed_tokens, h->s->model(), now);
+    fill_cost(out, gpu, c);
+  });
+}
+
+int e2_match(e2_handle* h, const int32_t* seq, int64_t len, int64_t* matched_len,
+             int64_t* cached_len, int64_t* per_gpu) {
+  return guard(h, [&] {
+    TokenSeq p(seq, seq + len);
+    MatchResult m = h->s->mirror().match(p);
+    if (matched_len) *matched_len = m.matched_len;
+    if (cached_len) *cached_len = m.cached_len;
+    if (per_gpu) {
+      for (int g = 0; g < h->n; ++g) per_gpu[g] = m.matched_on(g);
+    }
+  });
+}
+
+int e2_export_size(e2_handle* h, int64_t* n_nodes, int64_t* n_tokens) {
+  return guard(h, [&] {
+    auto nodes = h->s->mirror().export_nodes();
+    int64_t t = 0;
+    for (auto& n : nodes) t += static_cast<int64_t>(n.edge.size());
+    *n_nodes = static_cast<int64_t>(nodes.size());
+    *n_tokens = t;
+  });
+}
+
+int e2_export(e2_handle* h, double now, e2_node* nodes, int32_t* tokens, double* last_access,
+              int64_t* hits) {
+  return guard(h, [&] {
+    auto snap = h->s->mirror().export_nodes();
+    const double horizon = h->s->config().history_window_ms;
+    int64_t off = 0;
+    for (size_t i = 0; i < snap.size(); ++i) {
+      const auto& s = snap[i];
+      if (nodes) {
+        e2_node& o = nodes[i];
+        o.id = s.id;
+        o.parent_id = s.parent_id;
+        o.edge_off = off;
+        o.edge_len = static_cast<int64_t>(s.edge.size());
+        o.caching_mask = 0;
+        for (GpuId g : s.caching_gpus) o.caching_mask |= (1ull << g);
+        o.last_access_mask = 0;
+        for (auto& [g, t] : s.last_access) o.last_access_mask |= (1ull << g);
+        o.pin_count = s.pin_count;
+      }
+      if (tokens) std::copy(s.edge.begin(), s.edge.end(), tokens + off);
+      off += static_cast<int64_t>(s.edge.size());
+      for (int g = 0; g < h->n; ++g) {
+        if (last_access) {
+          auto it = s.last_access.find(g);
+          last_access[i * h->n + g] = it == s.last_access.end() ? 0.0 : it->second;
+        }
+        if (hits) {
+          int64_t c = 0;
+          auto it = s.hits.find(g);
+          if (it != s.hits.end()) {
+            for (double t : it->second) c += (t >= now - horizon) ? 1 : 0;
+          }
+          hits[i * h->n + g] = c;
+        }
+      }
+    }
+  });
+}
+
+int e2_debug_dump(e2_handle* h, double now, char* buf, size_t cap, size_t* needed) {
+  return guard(h, [&] {
+    std::string s = h->s->mirror().debug_dump(now, h->s->config().history_window_ms);
+    if (needed) *needed = s.size();
+    if (buf && cap > 0) {
+      size_t k = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
+  });
+}
+
+int e2_window_sizes(e2_handle* h, int32_t gpu, double now, int64_t* n_scheduled,
+                    int64_t* n_completed, int64_t* inflight_cached, int64_t* inflight_prompt) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    ClusterSnapshot snap = h->s->snapshot(now);
+    const auto& g = snap.gpus[gpu];
+    if (n_scheduled) *n_scheduled = static_cast<int64_t>(g.scheduled.size());
+    if (n_completed) *n_completed = static_cast<int64_t>(g.completed.size());
+    if (inflight_cached) *inflight_cached = g.inflight_cached;
+    if (inflight_prompt) *inflight_prompt = g.inflight_prompt;
+  });
+}
+
+// The generalised criterion-7 loop (acceptance_main.cpp:367-416), driving the
+// reference through its public API only.
+int e2_replay(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const int64_t* ids,
+              const double* arrivals, const int64_t* output_lens, int64_t n,
+              const e2_driver_cfg* drv, e2_decision* out, e2_cost* costs, double* ratios,
+              int64_t* n_done) {
+  if (n_done) *n_done = 0;
+  GlobalScheduler& s = *h->s;
+  std::vector<std::deque<std::pair<int64_t, int64_t>>> fifo(h->n);
+  double now = 0;
+  int64_t i = 0;
+  int rc = guard(h, [&] {
+    for (i = 0; i < n; ++i) {
+      now = std::max(now, arrivals[i]);
+      Request r;
+      r.id = ids[i];
+      r.arrival_ms = arrivals[i];
+      r.prompt.assign(tokens + offsets[i], tokens + offsets[i + 1]);
+      r.output_len = output_lens[i];
+      const int64_t matched = s.mirror().match(r.prompt).matched_len;
+      const Decision d = s.schedule_request(r, now);
+      fill_decision(d, matched, h->n, out ? out + i : nullptr,
+                    costs ? costs + i * (h->n + 1) : nullptr, ratios ? ratios + i * h->n : nullptr);
+      if (drv->prefill_cached) s.note_prefill_cached(r.prompt, d.gpu, now);
+      if (drv->eviction == E2_EVICT_FIFO_TAIL) {
+        fifo[d.gpu].push_back({i, static_cast<int64_t>(r.prompt.size()) - drv->trunk_len});
+        while (s.mirror().cached_tokens(d.gpu) > drv->high_water && !fifo[d.gpu].empty()) {
+          auto [k, tail] = fifo[d.gpu].front();
+          fifo[d.gpu].pop_front();
+          EvictedRange range;
+          range.seq.assign(tokens + offsets[k], tokens + offsets[k + 1]);
+          range.tail_len = tail;
+          s.note_eviction(range, d.gpu, now);
+        }
+      } else if (drv->eviction == E2_EVICT_MIRROR_LRU) {
+        const int64_t cached = s.mirror().cached_tokens(d.gpu);
+        if (cached > drv->high_water) {
+          EvictionPlan plan = s.mirror().plan_eviction(d.gpu, cached - drv->high_water, {}, true);
+          std::vector<EvictedRange> ranges;
+          for (const auto& e : plan.entries) {
+            ranges.push_back({s.mirror().path_tokens(e.node), e.tokens});
+          }
+          for (const auto& rg : ranges) s.note_eviction(rg, d.gpu, now);
+        }
+      }
+      if (i >= drv->finish_lag) {
+        const int64_t k = i - drv->finish_lag;
+        s.note_finished(ids[k], now, output_lens[k]);
+      }
+    }
+  });
+  if (n_done) *n_done = i;
+  return rc;
+}
+
+int e2_replay_device(e2_handle* h, const int32_t*, const int64_t*, const int64_t*, const double*,
+                     const int64_t*, int64_t, const e2_driver_cfg*, e2_decision*, e2_cost*, double*,
+                     void*, int64_t*) {
+  h->err = "reference backend has no device path";
+  return E2_ERR_ARG;
+}
+
+int e2_profile_get(e2_handle* h, e2_profile* out) {
+  (void)h;
+  std::memset(out, 0, sizeof(*out));
+  return E2_OK;
+}
+
+int e2_profile_reset(e2_handle*, int32_t) { return E2_OK; }
+
+void e2_workload_default(int32_t archetype, e2_workload_spec* out) {
+  std::memset(out, 0, sizeof(*out));
+  Archetype a = Archetype::Custom;
+  switch (archetype) {
+    case E2_ARCH_TOOLBENCH: a = Archetype::Toolbench; break;
+    case E2_ARCH_EMBODIED: a = Archetype::EmbodiedAgent; break;
+    case E2_ARCH_PROGRAMMING: a = Archetype::Programming; break;
+    case E2_ARCH_VIDEO_QA: a = Archetype::VideoQa; break;
+    case E2_ARCH_DOC_QA: a = Archetype::DocQa; break;
+    default: a = Archetype::Custom; break;
+  }
+  WorkloadSpec s = WorkloadSpec::archetype_default(a);
+  out->archetype = archetype;
+  out->zipf = s.popularity == Popularity::Zipf ? 1 : 0;
+  out->request_count = s.request_count;
+  out->system_prompt_len = s.system_prompt_len;
+  out->branch_count = s.branch_count;
+  out->branch_len = s.branch_len;
+  out->branch_len_max = s.branch_len;
+  out->zipf_s = s.zipf_s;
+  out->unique_min = s.unique_suffix_len.min;
+  out->unique_max = s.unique_suffix_len.max;
+  out->output_min = s.output_len.min;
+  out->output_max = s.output_len.max;
+  out->requests_per_group = s.requests_per_group;
+  out->chain_mean_len = s.chain_mean_len;
+  out->observation_len = s.observation_len;
+}
+
+int e2_generate(const e2_workload_spec* spec, uint64_t seed, double rps, uint64_t arrival_seed,
+                int64_t* n_requests, int64_t* n_tokens, int32_t* tokens, int64_t* offsets,
+                int64_t* ids, double* arrivals, int64_t* output_lens) {
+  Archetype a;
+  switch (spec->archetype) {
+    case E2_ARCH_CUSTOM: a = Archetype::Custom; break;
+    case E2_ARCH_TOOLBENCH: a = Archetype::Toolbench; break;
+    case E2_ARCH_EMBODIED: a = Archetype::EmbodiedAgent; break;
+    case E2_ARCH_PROGRAMMING: a = Archetype::Programming; break;
+    case E2_ARCH_VIDEO_QA: a = Archetype::VideoQa; break;
+    case E2_ARCH_DOC_QA: a = Archetype::DocQa; break;
+    default: g_create_err = "archetype not in the reference"; return E2_ERR_ARG;
+  }
+  if (spec->branch_len_max > spec->branch_len) {
+    g_create_err = "variable trunk lengths are not a reference feature";
+    return E2_ERR_ARG;
+  }
+  try {
+    WorkloadSpec s;
+    s.archetype = a;
+    s.request_count = spec->request_count;
+    s.system_prompt_len = spec->system_prompt_len;
+    s.branch_count = static_cast<int>(spec->branch_count);
+    s.branch_len = spec->branch_len;
+    s.popularity = spec->zipf ? Popularity::Zipf : Popularity::Uniform;
+    s.zipf_s = spec->zipf_s;
+    s.unique_suffix_len = {spec->unique_min, spec->unique_max};
+    s.output_len = {spec->output_min, spec->output_max};
+    s.requests_per_group = spec->requests_per_group;
+    s.chain_mean_len = spec->chain_mean_len;
+    s.observation_len = spec->observation_len;
+    Corpus c = generate(s, seed);
+    assign_poisson_arrivals(c, rps, arrival_seed);
+    int64_t nt = 0;
+    for (auto& e : c) nt += static_cast<int64_t>(e.prompt.size());
+    *n_requests = static_cast<int64_t>(c.size());
+    *n_tokens = nt;
+    if (!tokens) return E2_OK;
+    int64_t off = 0;
+    for (size_t i = 0; i < c.size(); ++i) {
+      offsets[i] = off;
+      std::copy(c[i].prompt.begin(), c[i].prompt.end(), tokens + off);
+      off += static_cast<int64_t>(c[i].prompt.size());
+      ids[i] = c[i].id;
+      arrivals[i] = *c[i].arrival_ms;
+      output_lens[i] = c[i].output_len;
+    }
+    offsets[c.size()] = off;
+    return E2_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return E2_ERR_CONFIG;
+  }
+}
+
+}  // extern "C"

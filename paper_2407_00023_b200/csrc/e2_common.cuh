@@ -1,0 +1,121 @@
+// e2_common.cuh — SIMT-generic primitives shared by every kernel.
+//
+// Device build (nvcc, sm_100a): code runs as one 32-lane warp; scalar control
+// logic is executed redundantly by all lanes (uniform values), single writes
+// go through lane 0 followed by __syncwarp, and the warp-cooperative pieces
+// (child-table probes, LRU page edits, per-instance cost lanes) use
+// ballot/shuffle.
+//
+// Host emulation build (E2_HOSTSIM, g++; TEST-ONLY, never linked into the
+// product library): the same source with a warp width of 1, so the CPU test
+// suite can exercise the engine's control logic without a GPU.
+#pragma once
+
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__CUDACC__) && !defined(E2_HOSTSIM)
+#define E2_DEVICE_BUILD 1
+#define E2_HD __device__ __forceinline__
+#define E2_HDX __host__ __device__ __forceinline__
+#define E2_D __device__ __forceinline__
+#define E2_DNI __device__ __noinline__
+#else
+#define E2_DEVICE_BUILD 0
+#define E2_HD inline
+#define E2_HDX inline
+#define E2_D inline
+#define E2_DNI
+#endif
+
+namespace e2 {
+
+typedef int64_t i64;
+typedef uint64_t u64;
+typedef int32_t i32;
+typedef uint32_t u32;
+
+constexpr u32 kNil = 0xffffffffu;
+constexpr u32 kRoot = 0;
+constexpr int kMaxG = 64;
+
+#if E2_DEVICE_BUILD
+constexpr int kWidth = 32;
+E2_D int lane() { return (int)(threadIdx.x & 31); }
+E2_D void wsync() { __syncwarp(); }
+E2_D u32 ballot(bool p) { return __ballot_sync(0xffffffffu, p); }
+E2_D bool any(bool p) { return __any_sync(0xffffffffu, p); }
+template <typename T>
+E2_D T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+E2_D int ffs32(u32 m) { return __ffs((int)m) - 1; }
+E2_D int popc32(u32 m) { return __popc(m); }
+E2_D int popc64(u64 m) { return __popcll(m); }
+E2_D int ffs64(u64 m) { return __ffsll((long long)m) - 1; }
+// Exact IEEE double ops with explicit rounding so nvcc never contracts a*b+c
+// into an FMA: the reference's bits are computed unfused (SURVEY 7 hard part 4).
+E2_D double dmul(double a, double b) { return __dmul_rn(a, b); }
+E2_D double dadd(double a, double b) { return __dadd_rn(a, b); }
+E2_D double dsub(double a, double b) { return __dsub_rn(a, b); }
+E2_D double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+E2_D double i2d(i64 v) { return __ll2double_rn((long long)v); }
+#else
+constexpr int kWidth = 1;
+inline int lane() { return 0; }
+inline void wsync() {}
+inline u32 ballot(bool p) { return p ? 1u : 0u; }
+inline bool any(bool p) { return p; }
+template <typename T>
+inline T shfl(T v, int) { return v; }
+inline int ffs32(u32 m) { return m ? __builtin_ctz(m) : -1; }
+inline int popc32(u32 m) { return __builtin_popcount(m); }
+inline int popc64(u64 m) { return __builtin_popcountll(m); }
+inline int ffs64(u64 m) { return m ? __builtin_ctzll(m) : -1; }
+inline double dmul(double a, double b) {
+  volatile double r = a * b;
+  return r;
+}
+inline double dadd(double a, double b) {
+  volatile double r = a + b;
+  return r;
+}
+inline double dsub(double a, double b) {
+  volatile double r = a - b;
+  return r;
+}
+inline double ddiv(double a, double b) {
+  volatile double r = a / b;
+  return r;
+}
+inline double i2d(i64 v) { return (double)v; }
+#endif
+
+E2_HD bool lane0() { return lane() == 0; }
+
+template <typename T>
+E2_HDX T min_(T a, T b) { return a < b ? a : b; }
+template <typename T>
+E2_HDX T max_(T a, T b) { return a > b ? a : b; }
+
+// Bit pattern of a non-negative double is monotone as an unsigned integer;
+// last_access values are always >= +0 (prefix_tree.cpp:21-24, 48-49).
+E2_HDX u64 dbits(double d) {
+  u64 u;
+  memcpy(&u, &d, 8);
+  return u;
+}
+E2_HDX double bitsd(u64 u) {
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+}
+
+E2_HDX u64 mix64(u64 x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+}  // namespace e2

@@ -1,0 +1,725 @@
+// e2_engine.cuh — the serial E2 semantics (decide + commit + callbacks +
+// batched driver) executed by one warp over the HBM-resident state.
+//
+// Every operation reproduces one reference call with identical state
+// effects; floating point uses explicit round-to-nearest intrinsics in the
+// reference's operation order.  Token comparisons never happen here: every
+// walk is given its matched length by the batched match kernels (K1 + the
+// intra-batch leader rounds, e2_match.cuh), so a walk costs one child-table
+// probe per tree level.
+#pragma once
+
+#include "e2_tree.cuh"
+
+namespace e2 {
+
+// Warp-shared per-decision scratch (shared memory on device).
+struct Scr {
+  double loads[kMaxG];
+  double ratios[kMaxG];
+  i64 ext[kMaxG];
+  i32 cgpu[kMaxG + 1];
+  i32 cinf[kMaxG + 1];
+  double cL[kMaxG + 1], cM[kMaxG + 1], cP[kMaxG + 1];
+  i32 n_costs;
+  i32 pad;
+};
+
+// Result of a node-level walk with a known matched length.
+struct Walk {
+  u32 last;       // deepest node touched (kRoot when nothing matched)
+  i64 last_m;     // tokens matched inside `last`
+  i64 cached_len; // Σ spans cached somewhere (prefix_tree.cpp:104-106)
+  u64 present;    // gpus with a per_gpu_matched_len entry (first span's set)
+  u32 first;      // first-level node (kNil when nothing matched)
+  bool ok;
+};
+
+// ---------------------------------------------------------------------------
+// Load windows — LoadWindow (cost_model.cpp:20-73).  Single-lane.
+// ---------------------------------------------------------------------------
+E2_HD u64 wslot(const Dev& d, int g, u64 i) { return (u64)g * d.wcap + (i & (d.wcap - 1)); }
+
+// hits(n, g) counts in-window requests placed on g whose prompt passes
+// through n: undo a request's stamps when it leaves g's window.
+E2_HD void hits_dec_chain(const Dev& d, u32 tail, int g) {
+  const int G = d.cfg.G;
+  for (u32 n = tail; n != kRoot && n != kNil; n = d.hdr[n].parent) d.hits[(u64)n * G + g] -= 1;
+}
+
+// prune (cost_model.cpp:31-42): inclusive horizon, t >= now - H survives.
+E2_HD void win_prune(const Dev& d, Hot* h, int g, double now) {
+  const double cutoff = dsub(now, d.cfg.H);
+  u64 hd = h->ws_head[g], tl = h->ws_tail[g];
+  while (hd < tl) {
+    u64 i = wslot(d, g, hd);
+    if (!(d.ws_t[i] < cutoff)) break;
+    const i64 m = d.ws_missed[i];
+    h->ws_missed_sum[g] -= m;
+    if (m > 0) h->ws_missed_nz[g] -= 1;
+    hits_dec_chain(d, d.ws_slot[i], g);
+    hd++;
+  }
+  h->ws_head[g] = hd;
+  u64 ch = h->wc_head[g], ct = h->wc_tail[g];
+  while (ch < ct) {
+    u64 i = wslot(d, g, ch);
+    if (!(d.wc_t[i] < cutoff)) break;
+    h->wc_output_sum[g] -= d.wc_out[i];
+    ch++;
+  }
+  h->wc_head[g] = ch;
+}
+
+// load_ms (cost_model.cpp:65-73) — prefill folded from integer sums, decode
+// = count * (c2 * avg_output).
+E2_HD double win_load(const Dev& d, Hot* h, int g, double now) {
+  win_prune(d, h, g, now);
+  const Cfg& c = d.cfg;
+  const i64 nsched = (i64)(h->ws_tail[g] - h->ws_head[g]);
+  const i64 ncomp = (i64)(h->wc_tail[g] - h->wc_head[g]);
+  double prefill = dadd(dmul(c.c0, i2d(h->ws_missed_nz[g])), dmul(c.c1, i2d(h->ws_missed_sum[g])));
+  double avg = ncomp == 0 ? i2d(c.default_out) : ddiv(i2d(h->wc_output_sum[g]), i2d(ncomp));
+  double decode = dmul(i2d(nsched), dmul(c.c2, avg));
+  return dadd(prefill, decode);
+}
+
+E2_HD bool win_add_sched(const Dev& d, Hot* h, int g, double now, i64 missed, i64 est, u32 tail) {
+  u64 t = h->ws_tail[g];
+  if (t - h->ws_head[g] >= d.wcap) {
+    set_err(h, kErrCapacity, kWhyWindowCap);
+    return false;
+  }
+  u64 i = wslot(d, g, t);
+  d.ws_t[i] = now;
+  d.ws_missed[i] = missed;
+  d.ws_est[i] = est;
+  d.ws_slot[i] = tail;
+  h->ws_tail[g] = t + 1;
+  h->ws_missed_sum[g] += missed;
+  if (missed > 0) h->ws_missed_nz[g] += 1;
+  return true;
+}
+
+E2_HD bool win_add_comp(const Dev& d, Hot* h, int g, double now, i64 out) {
+  u64 t = h->wc_tail[g];
+  if (t - h->wc_head[g] >= d.wcap) {
+    set_err(h, kErrCapacity, kWhyWindowCap);
+    return false;
+  }
+  u64 i = wslot(d, g, t);
+  d.wc_t[i] = now;
+  d.wc_out[i] = out;
+  h->wc_tail[g] = t + 1;
+  h->wc_output_sum[g] += out;
+  return true;
+}
+
+E2_HD double prefill_time(const Cfg& c, i64 missed) {
+  if (missed <= 0) return 0.0;
+  return dadd(c.c0, dmul(c.c1, i2d(missed)));
+}
+
+// ---------------------------------------------------------------------------
+// Eviction planning — PrefixTree::plan_eviction (prefix_tree.cpp:273-308).
+// Single-lane, read-only on the tree; per-instance scratch holds the
+// surfaced-parent work list (sorted) and the simulated cached-child counts.
+// visit(slot, tokens) is called per plan entry in plan order.
+// Returns freed tokens.
+// ---------------------------------------------------------------------------
+template <typename Visit>
+E2_HD i64 plan_eviction(const Dev& d, Hot* h, int g, i64 need, bool partial, Visit&& visit) {
+  if (need <= 0) return 0;
+  const int G = d.cfg.G;
+  const u32 half = d.scap / 2;
+  u32* s_slot = d.scr_slot + (u64)g * d.scap;  // [0,half): surfaced list, [half,scap): sim ccc
+  u64* s_la = d.scr_la + (u64)g * d.scap;
+  u64* s_id = d.scr_id + (u64)g * d.scap;
+  i64* s_val = d.scr_val + (u64)g * d.scap;
+  u32 ns = 0, nsurf_head = 0, nsim = 0;
+  const u32 nd = h->dir_n[g];
+  u32 k = 0, j = 0, page = kNil;
+  i32 pcnt = 0;
+  if (nd > 0) {
+    page = d.dir_page[dring(d, h, g, 0)];
+    pcnt = d.pg_n[page];
+  }
+  i64 freed = 0;
+  while (freed < need) {
+    bool have_a = page != kNil;
+    bool have_b = nsurf_head < ns;
+    if (!have_a && !have_b) break;
+    u32 v;
+    bool take_b = false;
+    if (have_a && have_b) {
+      u64 ai = (u64)page * kPage + j;
+      take_b = kless(s_la[nsurf_head], s_id[nsurf_head], d.pg_la[ai], d.pg_id[ai]);
+    } else {
+      take_b = have_b;
+    }
+    if (take_b) {
+      v = s_slot[nsurf_head++];
+    } else {
+      v = d.pg_slot[(u64)page * kPage + j];
+      if (++j >= (u32)pcnt) {
+        j = 0;
+        if (++k < nd) {
+          page = d.dir_page[dring(d, h, g, k)];
+          pcnt = d.pg_n[page];
+        } else {
+          page = kNil;
+        }
+      }
+    }
+    const i64 tok = d.hdr[v].edge_len;
+    const i64 remaining = need - freed;
+    if (partial && tok > remaining) {
+      visit(v, remaining);
+      freed += remaining;
+      break;
+    }
+    visit(v, tok);
+    freed += tok;
+    const u32 p = d.hdr[v].parent;
+    if (p != kNil && p != kRoot && cached_on(d, p, g)) {
+      u32 x = 0;
+      while (x < nsim && s_slot[half + x] != p) ++x;
+      i64 c;
+      if (x < nsim) {
+        c = s_val[half + x] - 1;
+      } else {
+        if (nsim >= d.scap - half) {
+          set_err(h, kErrCapacity, kWhyScratchCap);
+          break;
+        }
+        c = (i64)d.ccc[(u64)p * G + g] - 1;
+        s_slot[half + nsim] = p;
+        nsim++;
+      }
+      s_val[half + x] = c;
+      if (c == 0) {
+        // sorted insert into the pending part of the surfaced list
+        if (ns >= half) {
+          set_err(h, kErrCapacity, kWhyScratchCap);
+          break;
+        }
+        const u64 pla = la_bits(d, p, g), pid = d.hdr[p].id;
+        u32 pos = ns;
+        while (pos > nsurf_head && kless(pla, pid, s_la[pos - 1], s_id[pos - 1])) {
+          s_la[pos] = s_la[pos - 1];
+          s_id[pos] = s_id[pos - 1];
+          s_slot[pos] = s_slot[pos - 1];
+          --pos;
+        }
+        s_la[pos] = pla;
+        s_id[pos] = pid;
+        s_slot[pos] = p;
+        ns++;
+      }
+    }
+  }
+  return freed;
+}
+
+// load_cost (cost_model.cpp:75-100).  Single-lane.
+struct CostOut {
+  double L, M, P;
+  bool inf;
+};
+
+E2_HD CostOut cost_for(const Dev& d, Hot* h, int g, i64 missed, double now) {
+  CostOut o;
+  o.L = win_load(d, h, g, now);
+  o.P = prefill_time(d.cfg, missed);
+  o.M = 0.0;
+  o.inf = false;
+  const i64 free_tokens = d.cfg.cap - h->cached_tokens[g];
+  const i64 need = missed - free_tokens;
+  if (need > 0) {
+    const i64 total = (i64)(h->ws_tail[g] - h->ws_head[g]);  // scheduled_count (already pruned)
+    const Cfg& c = d.cfg;
+    const int G = c.G;
+    double M = 0.0;
+    i64 freed = plan_eviction(d, h, g, need, false, [&](u32 v, i64 tok) {
+      if (total > 0) {
+        const double nj = ddiv(i2d(d.hits[(u64)v * G + g]), i2d(total));
+        M = dadd(M, dmul(prefill_time(c, tok), nj));
+      }
+    });
+    o.M = M;
+    o.inf = freed < need;
+  }
+  return o;
+}
+
+// ---------------------------------------------------------------------------
+// Walks (warp-wide).  `L` = matched length of the sequence against the
+// current tree, from the batched match; prefix_tree.cpp:79-114.
+// ---------------------------------------------------------------------------
+E2_D Walk walk_known(const Dev& d, const i32* seq, i64 L, i64* ext) {
+  Walk w;
+  w.last = kRoot;
+  w.last_m = 0;
+  w.cached_len = 0;
+  w.present = 0;
+  w.first = kNil;
+  w.ok = true;
+  const int G = d.cfg.G;
+  for (int g = lane(); g < G; g += kWidth) ext[g] = 0;
+  u64 alive = 0;
+  bool first_span = true;
+  i64 pos = 0;
+  u32 cur = kRoot;
+  while (pos < L) {
+    u32 ch = child_lookup(d, cur, seq[pos]);
+    if (ch == kNil) {
+      w.ok = false;
+      break;
+    }
+    const i64 len = d.hdr[ch].edge_len;
+    const i64 m = min_(len, L - pos);
+    const u64 cm = d.cmask[ch];
+    if (first_span) {
+      alive = cm;
+      w.present = cm;
+      w.first = ch;
+      first_span = false;
+    } else {
+      alive &= cm;
+    }
+    for (int g = lane(); g < G; g += kWidth)
+      if ((alive >> g) & 1ull) ext[g] += m;
+    if (cm != 0) w.cached_len += m;
+    pos += m;
+    cur = ch;
+    w.last = ch;
+    w.last_m = m;
+    if (m < len) break;
+  }
+  wsync();
+  return w;
+}
+
+// ensure_path (prefix_tree.cpp:156-185) given the walk of the same sequence.
+// Returns the node whose edge ends exactly at |seq| (kNil on error).
+E2_D u32 ensure_path(const Dev& d, Hot* h, i64 seq_off, i64 n, i64 L, const Walk& w) {
+  u32 cur = (L == 0) ? kRoot : w.last;
+  if (L > 0 && w.last_m < (i64)d.hdr[w.last].edge_len) {
+    cur = split_node(d, h, w.last, (u32)w.last_m);
+    if (cur == kNil) return kNil;
+  }
+  if (L == n) return cur;
+  return new_leaf(d, h, cur, seq_off + L, (u32)(n - L), (u32)L);
+}
+
+// ---------------------------------------------------------------------------
+// Redirect upkeep — update_redirects (global_scheduler.cpp:194-219).  Warp-wide.
+// ---------------------------------------------------------------------------
+E2_D void update_redirects(const Dev& d, Hot* h, Scr* s, double now) {
+  const int G = d.cfg.G;
+  for (int g = lane(); g < G; g += kWidth) s->loads[g] = win_load(d, h, g, now);
+  wsync();
+  if (lane0()) {
+    const double th = d.cfg.th_bal;
+    for (int src = 0; src < G; ++src) {
+      int dst = h->redirect[src];
+      if (dst >= 0 && s->loads[src] <= dmul(th, s->loads[dst])) h->redirect[src] = -1;
+    }
+    int hi = 0, lo = 0;
+    for (int g = 1; g < G; ++g) {
+      if (s->loads[g] > s->loads[hi]) hi = g;
+      if (s->loads[g] < s->loads[lo]) lo = g;
+    }
+    if (!(hi == lo || !(s->loads[hi] > dmul(th, s->loads[lo])))) {
+      if (h->redirect[hi] != lo) {
+        h->redirect[hi] = lo;
+        h->stats[kStInstalls]++;
+      }
+    }
+  }
+  wsync();
+}
+
+// pick_min_cost (global_scheduler.cpp:54-74) over s->c*[0, n).
+E2_HD int pick_min(const Scr* s, int n) {
+  int best = -1;
+  double bt = 0;
+  for (int i = 0; i < n; ++i) {
+    if (s->cinf[i]) continue;
+    double t = dadd(dadd(s->cL[i], s->cM[i]), s->cP[i]);
+    if (best < 0 || t < bt) {
+      best = s->cgpu[i];
+      bt = t;
+    }
+  }
+  if (best >= 0) return best;
+  for (int i = 0; i < n; ++i) {
+    double t = dadd(dadd(s->cL[i], s->cM[i]), s->cP[i]);
+    if (best < 0 || t < bt) {
+      best = s->cgpu[i];
+      bt = t;
+    }
+  }
+  return best;
+}
+
+struct Dec {
+  i32 branch, gpu, redirected, pre;
+  i64 cached_len, missed_len, moc, matched;
+  i32 has_ratios;
+  i32 ok;  // 0 = error raised
+};
+
+// decide (global_scheduler.cpp:76-158).  Warp-wide.  Fills s->c* and
+// s->ratios; w receives the walk for a following commit.
+E2_D Dec decide(const Dev& d, Hot* h, Scr* s, const i32* seq, i64 n, i64 L, double now, Walk& w) {
+  Dec r;
+  r.branch = 1;
+  r.gpu = -1;
+  r.redirected = 0;
+  r.pre = -1;
+  r.cached_len = 0;
+  r.missed_len = 0;
+  r.moc = 0;
+  r.matched = L;
+  r.has_ratios = 0;
+  r.ok = 1;
+  const int G = d.cfg.G;
+  if (lane0()) s->n_costs = 0;
+  wsync();
+  if (n > d.cfg.cap) {
+    if (lane0()) set_err(h, kErrNoAdmissible, kWhyPromptTooLong);
+    wsync();
+    r.ok = 0;
+    return r;
+  }
+  if (d.cfg.mode == 1) {
+    r.branch = 3;
+    r.gpu = (i32)(h->rr_next % G);
+    r.missed_len = n;
+    r.moc = n;
+    r.matched = 0;
+    return r;
+  }
+  if (lane0()) h->stats[kStTreeReads]++;
+  wsync();
+  w = walk_known(d, seq, L, s->ext);
+  if (!w.ok) {
+    if (lane0()) set_err(h, kErrSim, kWhyWalk);
+    wsync();
+    r.ok = 0;
+    return r;
+  }
+  // per_gpu_matched_len entries exist only for gpus caching the first span
+  for (int g = lane(); g < G; g += kWidth)
+    if (!((w.present >> g) & 1ull)) s->ext[g] = 0;
+  wsync();
+  r.cached_len = w.cached_len;
+  r.missed_len = n - w.cached_len;
+  if (r.missed_len < r.cached_len) {
+    r.branch = 0;
+    i64 best = 0;
+    for (int g = 0; g < G; ++g)
+      if (((w.present >> g) & 1ull) && s->ext[g] > best) best = s->ext[g];
+    // candidates in ascending gpu order; lanes evaluate their own instances
+    u64 cand = 0;
+    for (int g = 0; g < G; ++g)
+      if (((w.present >> g) & 1ull) && s->ext[g] == best) cand |= (1ull << g);
+    for (int g = lane(); g < G; g += kWidth) {
+      if ((cand >> g) & 1ull) {
+        int idx = popc64(cand & ((1ull << g) - 1));
+        CostOut c = cost_for(d, h, g, n - s->ext[g], now);
+        s->cgpu[idx] = g;
+        s->cL[idx] = c.L;
+        s->cM[idx] = c.M;
+        s->cP[idx] = c.P;
+        s->cinf[idx] = c.inf ? 1 : 0;
+      }
+    }
+    wsync();
+    int nc = popc64(cand);
+    int gpu = pick_min(s, nc);
+    if (gpu >= 0 && h->redirect[gpu] >= 0 && h->redirect[gpu] != gpu) {
+      const int t = h->redirect[gpu];
+      int ti = -1;
+      for (int i = 0; i < nc; ++i)
+        if (s->cgpu[i] == t) ti = i;
+      if (ti < 0) {
+        if (lane0()) {
+          CostOut c = cost_for(d, h, t, n - s->ext[t], now);
+          s->cgpu[nc] = t;
+          s->cL[nc] = c.L;
+          s->cM[nc] = c.M;
+          s->cP[nc] = c.P;
+          s->cinf[nc] = c.inf ? 1 : 0;
+        }
+        wsync();
+        ti = nc;
+        nc++;
+      }
+      if (!s->cinf[ti]) {
+        r.redirected = 1;
+        r.pre = gpu;
+        gpu = t;
+      }
+    }
+    if (lane0()) s->n_costs = nc;
+    wsync();
+    r.gpu = gpu;
+  } else {
+    r.has_ratios = 1;
+    for (int g = lane(); g < G; g += kWidth) {
+      const i64 ip = h->inflight_prompt[g];
+      s->ratios[g] = ip <= 0 ? 0.0 : ddiv(i2d(h->inflight_cached[g]), i2d(ip));
+    }
+    wsync();
+    int max_g = -1;
+    double max_r = -1.0;
+    for (int g = 0; g < G; ++g) {
+      if (s->ratios[g] > max_r) {
+        max_r = s->ratios[g];
+        max_g = g;
+      }
+    }
+    if (d.cfg.pd_balance && max_r > d.cfg.imbal) {
+      r.branch = 2;
+      r.gpu = max_g;
+    } else {
+      r.branch = 1;
+      for (int g = lane(); g < G; g += kWidth) {
+        CostOut c = cost_for(d, h, g, n - s->ext[g], now);
+        s->cgpu[g] = g;
+        s->cL[g] = c.L;
+        s->cM[g] = c.M;
+        s->cP[g] = c.P;
+        s->cinf[g] = c.inf ? 1 : 0;
+      }
+      wsync();
+      if (lane0()) s->n_costs = G;
+      wsync();
+      r.gpu = pick_min(s, G);
+    }
+  }
+  if (h->err) {
+    r.ok = 0;
+    return r;
+  }
+  if (r.gpu < 0 || r.gpu >= G) {
+    if (lane0()) set_err(h, kErrSim, kWhyNotContiguous);
+    wsync();
+    r.ok = 0;
+    return r;
+  }
+  r.moc = n - s->ext[r.gpu];
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Inflight map: request id -> placement (global_scheduler.hpp:129-135).
+// Single-lane; linear probing with backward-shift deletion.
+// ---------------------------------------------------------------------------
+E2_HD u64 inf_find(const Dev& d, i64 id, bool& found) {
+  u64 i = mix64((u64)id) & d.inf_mask;
+  for (u64 k = 0; k <= d.inf_mask; ++k, i = (i + 1) & d.inf_mask) {
+    i64 key = d.inf_key[i];
+    if (key == id && key != kNoInflight) {
+      found = true;
+      return i;
+    }
+    if (key == kNoInflight) {
+      found = false;
+      return i;
+    }
+  }
+  found = false;
+  return ~0ull;
+}
+
+E2_HD void inf_erase_at(const Dev& d, u64 i) {
+  u64 j = i;
+  for (;;) {
+    j = (j + 1) & d.inf_mask;
+    i64 key = d.inf_key[j];
+    if (key == kNoInflight) break;
+    u64 home = mix64((u64)key) & d.inf_mask;
+    // move j into the hole at i if home is not cyclically in (i, j]
+    bool in_range = (i <= j) ? (home > i && home <= j) : (home > i || home <= j);
+    if (!in_range) {
+      d.inf_key[i] = key;
+      d.inf_gpu[i] = d.inf_gpu[j];
+      d.inf_cached[i] = d.inf_cached[j];
+      d.inf_prompt[i] = d.inf_prompt[j];
+      d.inf_arr[i] = d.inf_arr[j];
+      d.inf_root[i] = d.inf_root[j];
+      i = j;
+    }
+  }
+  d.inf_key[i] = kNoInflight;
+}
+
+// commit (global_scheduler.cpp:160-175).  Warp-wide.  Returns the tail slot.
+E2_D u32 commit(const Dev& d, Hot* h, i64 seq_off, const i32* seq, i64 n, i64 L, const Walk& w,
+                const Dec& r, i64 req_id, double arrival, double now) {
+  if (d.cfg.mode == 1) {
+    if (lane0()) h->rr_next++;
+    wsync();
+    return kNil;
+  }
+  if (n == 0) {
+    if (lane0()) set_err(h, kErrSim, kWhyEmptyInsert);
+    wsync();
+    return kNil;
+  }
+  (void)seq;
+  u32 tail = ensure_path(d, h, seq_off, n, L, w);
+  if (tail == kNil || h->err) return kNil;
+  const int g = r.gpu;
+  const int G = d.cfg.G;
+  // record_hit bottom-up (prefix_tree.cpp:193-196)
+  u32 first = tail;
+  for (u32 x = tail; x != kRoot; x = d.hdr[x].parent) {
+    first = x;
+    if (lane0()) d.hits[(u64)x * G + g] += 1;
+    wsync();
+    touch_la(d, h, x, g, now);
+  }
+  const u64 root_id = d.hdr[first].id;
+  wsync();
+  if (lane0()) {
+    win_add_sched(d, h, g, now, r.moc, d.cfg.default_out, tail);
+    h->inflight_cached[g] += r.cached_len;
+    h->inflight_prompt[g] += n;
+    bool found;
+    u64 i = inf_find(d, req_id, found);
+    if (i == ~0ull) {
+      set_err(h, kErrCapacity, kWhyInflightCap);
+    } else {
+      if (!found) {
+        h->inflight_n++;
+        if ((u64)h->inflight_n * 2 > d.inf_mask + 1) set_err(h, kErrCapacity, kWhyInflightCap);
+      }
+      d.inf_key[i] = req_id;
+      d.inf_gpu[i] = g;
+      d.inf_cached[i] = r.cached_len;
+      d.inf_prompt[i] = n;
+      d.inf_arr[i] = arrival;
+      d.inf_root[i] = root_id;
+    }
+  }
+  wsync();
+  return tail;
+}
+
+// Stats (global_scheduler.cpp:183-189).
+E2_D void count_stats(Hot* h, const Dec& r) {
+  if (lane0()) {
+    h->stats[r.branch == 0 ? kStExploit : r.branch == 1 ? kStExplore : r.branch == 2 ? kStPressure : kStRoundRobin]++;
+    if (r.redirected) h->stats[kStRedirected]++;
+  }
+  wsync();
+}
+
+// mark_cached_path bottom-up part (prefix_tree.cpp:203-211) from a known tail.
+E2_D void mark_cached_chain(const Dev& d, Hot* h, u32 tail, int g, double now) {
+  for (u32 x = tail; x != kRoot; x = d.hdr[x].parent) {
+    set_cached(d, h, x, g);
+    touch_la(d, h, x, g, now);
+  }
+}
+
+// note_finished (global_scheduler.cpp:361-369).  Warp-wide.
+E2_D void note_finished(const Dev& d, Hot* h, i64 id, double now, i64 out) {
+  if (lane0()) {
+    bool found;
+    u64 i = inf_find(d, id, found);
+    if (found) {
+      const int g = d.inf_gpu[i];
+      win_add_comp(d, h, g, now, out);
+      h->inflight_cached[g] -= d.inf_cached[i];
+      h->inflight_prompt[g] -= d.inf_prompt[i];
+      inf_erase_at(d, i);
+      h->inflight_n--;
+    }
+  }
+  wsync();
+}
+
+// uncache_suffix (prefix_tree.cpp:237-271) for a sequence whose matched
+// length M is known.  Warp-wide.  Returns tokens uncached.
+E2_D i64 uncache_suffix(const Dev& d, Hot* h, const i32* seq, i64 n, i64 M, i64 tail_len, int g) {
+  if (n == 0 || tail_len <= 0) return 0;
+  const i64 end = min_(n, M);
+  i64 start = n - tail_len;
+  if (start < 0) start = 0;
+  if (start >= end) return 0;
+  // walk down, aligning splits; `bottom` ends at `end`
+  i64 off = 0;
+  u32 cur = kRoot, bottom = kNil;
+  while (off < end) {
+    u32 ch = child_lookup(d, cur, seq[off]);
+    if (ch == kNil) {
+      if (lane0()) set_err(h, kErrSim, kWhyWalk);
+      wsync();
+      return 0;
+    }
+    const i64 len = d.hdr[ch].edge_len;
+    const i64 m = min_(len, M - off);
+    u32 node = ch;
+    if (m < len) {
+      node = split_node(d, h, ch, (u32)m);  // keep the part on seq's path
+      if (node == kNil) return 0;
+    }
+    const i64 node_end = off + m;
+    if (node_end > start && off < start) {
+      // split at start: the slot keeps the suffix, which is the target
+      u32 pre = split_node(d, h, node, (u32)(start - off));
+      if (pre == kNil) return 0;
+    }
+    bottom = node;
+    cur = node;
+    off = node_end;
+    if (m < len) break;
+  }
+  // clear deepest-first: bottom up to the node starting at `start`
+  i64 freed = 0;
+  for (u32 x = bottom; x != kRoot && x != kNil; x = d.hdr[x].parent) {
+    const i64 x_end = (i64)d.hdr[x].depth + d.hdr[x].edge_len;
+    if (x_end <= start) break;
+    if (cached_on(d, x, g)) {
+      freed += d.hdr[x].edge_len;
+      clear_cached(d, h, x, g);
+    }
+  }
+  return freed;
+}
+
+// Mirror-LRU eviction: plan_eviction(g, over, {}, partial)
+// then note_eviction for every entry, ranges built before any is applied.
+E2_D void evict_lru(const Dev& d, Hot* h, int g, i64 over) {
+  if (lane0()) {
+    u32 nv = 0;
+    plan_eviction(d, h, g, over, true, [&](u32 v, i64 tok) {
+      if (nv < d.vcap) {
+        d.vic_slot[nv] = v;
+        d.vic_tok[nv] = tok;
+        nv++;
+      } else {
+        set_err(h, kErrCapacity, kWhyScratchCap);
+      }
+    });
+    d.scr_val[(u64)d.cfg.G * d.scap] = nv;  // count, in the spare scratch word
+  }
+  wsync();
+  const u32 nv = (u32)d.scr_val[(u64)d.cfg.G * d.scap];
+  for (u32 i = 0; i < nv && !h->err; ++i) {
+    u32 v = d.vic_slot[i];
+    const i64 tok = d.vic_tok[i];
+    const i64 len = d.hdr[v].edge_len;
+    if (tok < len) {
+      if (split_node(d, h, v, (u32)(len - tok)) == kNil) return;
+    }
+    clear_cached(d, h, v, g);
+  }
+}
+
+}  // namespace e2

@@ -1,0 +1,392 @@
+// e2_kernels.cuh — kernel bodies: the serial replay/op warp, K1 match, and
+// the leader-round grouping.  Included once by e2_lib.cu.
+#pragma once
+
+#include "e2_engine.cuh"
+#include "e2_match.cuh"
+#include "e2sched.h"
+
+namespace e2 {
+
+enum OpKind : i32 {
+  OP_SCHEDULE = 1,
+  OP_DECIDE,
+  OP_PREFILL,
+  OP_EVICT,
+  OP_FINISHED,
+  OP_LOAD_COST,
+  OP_GPU_LOAD,
+  OP_MATCH,
+  OP_EXPIRE_ALL,
+  OP_WINDOW,
+  OP_INFLIGHT_GET,
+  OP_PRUNE_DEAD,
+  OP_MARK_NODE,      // autoscale: mark_cached_node(slot, gpu, now)
+  OP_MARK_SUBTREE,   // autoscale: mark_cached_subtree
+  OP_UNCACHE_SUBTREE // autoscale: uncache_subtree
+};
+
+struct OpDesc {
+  i32 kind;
+  i32 gpu;
+  i64 off;  // arena offset of the sequence
+  i64 len;
+  i64 L;    // matched length from K1
+  i64 x;    // tail_len / missed / output_len / slot
+  i64 id;
+  double now;
+  double arr;
+};
+
+struct ApiOut {
+  e2_decision dec;
+  e2_cost costs[kMaxG + 1];
+  double ratios[kMaxG];
+  i64 ext[kMaxG];
+  double v;
+  i64 i0, i1, i2, i3;
+  u64 u0;
+};
+
+struct SerialArgs {
+  i32 kind;  // 0 replay batch, 1 api op
+  i32 eviction, prefill;
+  i32 pad;
+  i64 base, n;
+  const i64* off;
+  const i64* len;
+  const i64* ids;
+  const double* arr;
+  const i64* outl;
+  const i64* L;  // batch-local
+  e2_decision* dec;
+  e2_cost* costs;
+  double* ratios;
+  i64 trunk, hw, lag;
+  OpDesc op;
+  ApiOut* out;
+};
+
+E2_D void write_decision(const Dev& d, const Scr* s, const Dec& r, i64 req_id, e2_decision* dec,
+                         e2_cost* costs, double* ratios) {
+  const int G = d.cfg.G;
+  const bool cost_path = (r.branch == 0 || r.branch == 1) && d.cfg.mode == 0;
+  const int nc = cost_path ? s->n_costs : 0;
+  if (lane0()) {
+    dec->request = req_id;
+    dec->branch = r.branch;
+    dec->gpu = r.gpu;
+    dec->redirected = r.redirected;
+    dec->pre_redirect_gpu = r.pre;
+    dec->n_costs = nc;
+    dec->has_ratios = r.has_ratios;
+    dec->cached_len = r.cached_len;
+    dec->missed_len = r.missed_len;
+    dec->missed_on_chosen = r.moc;
+    dec->matched_len = r.matched;
+  }
+  if (costs) {
+    for (int i = lane(); i < nc; i += kWidth) {
+      e2_cost c;
+      c.gpu = s->cgpu[i];
+      c.eviction_infeasible = s->cinf[i];
+      c.current_load_ms = s->cL[i];
+      c.eviction_ms = s->cM[i];
+      c.prefill_ms = s->cP[i];
+      costs[i] = c;
+    }
+  }
+  if (ratios && r.has_ratios) {
+    for (int g = lane(); g < G; g += kWidth) ratios[g] = s->ratios[g];
+  }
+  wsync();
+}
+
+// Dead-node removal (prefix_tree.cpp:357-378): a node goes when it is
+// uncached, childless and has no in-window hit on any instance; repeat until
+// a fixpoint (the reference removes bottom-up in one DFS).  Warp-wide.
+E2_D i64 prune_dead(const Dev& d, Hot* h) {
+  const int G = d.cfg.G;
+  i64 removed = 0;
+  bool again = true;
+  while (again) {
+    again = false;
+    const u32 used = h->slots_used;
+    for (u32 b = 1; b < used; b += kWidth) {
+      u32 s = b + (u32)lane();
+      bool dead = false;
+      if (s < used) {
+        const NodeHdr hd = d.hdr[s];
+        if (hd.edge_len > 0 && d.cmask[s] == 0 && d.nchild[s] == 0) {
+          dead = true;
+          for (int g = 0; g < G; ++g)
+            if (d.hits[(u64)s * G + g] != 0) dead = false;
+        }
+      }
+      u32 m = ballot(dead);
+      while (m) {
+        int j = ffs32(m);
+        m &= m - 1;
+        u32 x = b + (u32)j;
+        NodeHdr hx = d.hdr[x];
+        child_erase(d, h, hx.parent, hx.first_tok);
+        if (lane0()) {
+          d.nchild[hx.parent] -= 1;
+          NodeHdr z = hx;
+          z.edge_len = 0;
+          z.parent = kNil;
+          d.hdr[x] = z;
+          h->node_count--;
+        }
+        wsync();
+        removed++;
+        again = true;
+      }
+    }
+  }
+  return removed;
+}
+
+// Subtree walks for autoscale replication (global_scheduler.cpp:299-338):
+// children are found by scanning parents (rare path).
+E2_D void subtree_apply(const Dev& d, Hot* h, u32 root, int g, double now, bool mark) {
+  // iterative DFS using the victim scratch as a stack
+  u32 top = 0;
+  if (lane0()) d.vic_slot[0] = root;
+  wsync();
+  top = 1;
+  u32 order = 0;
+  // collect the subtree (preorder) into vic_slot, then apply
+  while (order < top) {
+    u32 x = d.vic_slot[order++];
+    const u32 used = h->slots_used;
+    for (u32 b = 1; b < used; b += kWidth) {
+      u32 s = b + (u32)lane();
+      bool ch = s < used && d.hdr[s].edge_len > 0 && d.hdr[s].parent == x;
+      u32 m = ballot(ch);
+      int cnt = popc32(m);
+      if (ch) {
+        int idx = popc32(m & ((1u << lane()) - 1));
+        d.vic_slot[top + idx] = s;
+      }
+      wsync();
+      top += cnt;
+    }
+  }
+  if (mark) {
+    for (u32 i = 0; i < top; ++i) {
+      u32 x = d.vic_slot[i];
+      if (x == kRoot) continue;
+      set_cached(d, h, x, g);
+      touch_la(d, h, x, g, now);
+    }
+  } else {
+    for (u32 i = top; i-- > 0;) {  // children before parents
+      u32 x = d.vic_slot[i];
+      if (x != kRoot) clear_cached(d, h, x, g);
+    }
+  }
+}
+
+E2_D void api_op(const Dev& d, Hot* h, Scr* s, const OpDesc& op, ApiOut* out) {
+  const int G = d.cfg.G;
+  const i32* seq = d.tok + op.off;
+  switch (op.kind) {
+    case OP_SCHEDULE:
+    case OP_DECIDE: {
+      const bool commit_it = op.kind == OP_SCHEDULE;
+      if (commit_it && d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(d, h, s, op.now);
+      Walk w;
+      Dec r = decide(d, h, s, seq, op.len, op.L, op.now, w);
+      if (!r.ok) return;
+      if (commit_it) {
+        commit(d, h, op.off, seq, op.len, op.L, w, r, op.id, op.arr, op.now);
+        if (h->err) return;
+        count_stats(h, r);
+      }
+      write_decision(d, s, r, op.id, &out->dec, out->costs, out->ratios);
+      break;
+    }
+    case OP_PREFILL: {
+      if (d.cfg.mode != 0 || op.len == 0) break;
+      Walk w = walk_known(d, seq, op.L, s->ext);
+      if (!w.ok) {
+        if (lane0()) set_err(h, kErrSim, kWhyWalk);
+        wsync();
+        return;
+      }
+      u32 tail = ensure_path(d, h, op.off, op.len, op.L, w);
+      if (tail == kNil || h->err) return;
+      mark_cached_chain(d, h, tail, op.gpu, op.now);
+      break;
+    }
+    case OP_EVICT: {
+      if (d.cfg.mode != 0) break;
+      i64 f = uncache_suffix(d, h, seq, op.len, op.L, op.x, op.gpu);
+      if (lane0()) out->i0 = f;
+      wsync();
+      break;
+    }
+    case OP_FINISHED:
+      note_finished(d, h, op.id, op.now, op.x);
+      break;
+    case OP_LOAD_COST: {
+      if (lane0()) {
+        CostOut c = cost_for(d, h, op.gpu, op.x, op.now);
+        out->costs[0].gpu = op.gpu;
+        out->costs[0].eviction_infeasible = c.inf ? 1 : 0;
+        out->costs[0].current_load_ms = c.L;
+        out->costs[0].eviction_ms = c.M;
+        out->costs[0].prefill_ms = c.P;
+      }
+      wsync();
+      break;
+    }
+    case OP_GPU_LOAD: {
+      if (lane0()) out->v = win_load(d, h, op.gpu, op.now);
+      wsync();
+      break;
+    }
+    case OP_MATCH: {
+      Walk w = walk_known(d, seq, op.L, s->ext);
+      for (int g = lane(); g < G; g += kWidth) out->ext[g] = ((w.present >> g) & 1ull) ? s->ext[g] : 0;
+      if (lane0()) {
+        out->i0 = op.L;
+        out->i1 = w.cached_len;
+      }
+      wsync();
+      break;
+    }
+    case OP_EXPIRE_ALL: {
+      for (int g = lane(); g < G; g += kWidth) win_prune(d, h, g, op.now);
+      wsync();
+      break;
+    }
+    case OP_WINDOW: {
+      if (lane0()) {
+        win_prune(d, h, op.gpu, op.now);
+        out->i0 = (i64)(h->ws_tail[op.gpu] - h->ws_head[op.gpu]);
+        out->i1 = (i64)(h->wc_tail[op.gpu] - h->wc_head[op.gpu]);
+        out->i2 = h->inflight_cached[op.gpu];
+        out->i3 = h->inflight_prompt[op.gpu];
+      }
+      wsync();
+      break;
+    }
+    case OP_INFLIGHT_GET: {
+      if (lane0()) {
+        bool found;
+        u64 i = inf_find(d, op.id, found);
+        out->i0 = found ? 1 : 0;
+        if (found) {
+          out->u0 = d.inf_root[i];
+          out->v = d.inf_arr[i];
+          out->i1 = d.inf_gpu[i];
+        }
+      }
+      wsync();
+      break;
+    }
+    case OP_PRUNE_DEAD: {
+      for (int g = lane(); g < G; g += kWidth) win_prune(d, h, g, op.now);
+      wsync();
+      i64 rm = prune_dead(d, h);
+      if (lane0()) out->i0 = rm;
+      wsync();
+      break;
+    }
+    case OP_MARK_NODE: {
+      u32 x = (u32)op.x;
+      if (x != kRoot) {
+        set_cached(d, h, x, op.gpu);
+        touch_la(d, h, x, op.gpu, op.now);
+      }
+      break;
+    }
+    case OP_MARK_SUBTREE:
+      subtree_apply(d, h, (u32)op.x, op.gpu, op.now, true);
+      break;
+    case OP_UNCACHE_SUBTREE:
+      subtree_apply(d, h, (u32)op.x, op.gpu, op.now, false);
+      break;
+    default:
+      break;
+  }
+}
+
+// One request of the generalised criterion-7 loop (e2sched.h, e2_replay).
+E2_D void replay_step(const Dev& d, Hot* h, Scr* s, const SerialArgs& a, i64 li) {
+  const int G = d.cfg.G;
+  const i64 r = a.base + li;
+  const i64 off = a.off[r], n = a.len[r];
+  const i32* seq = d.tok + off;
+  const double now = max_(h->drv_now, a.arr[r]);
+  if (lane0()) h->drv_now = now;
+  wsync();
+  if (d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(d, h, s, now);
+  Walk w;
+  Dec dec = decide(d, h, s, seq, n, a.L[li], now, w);
+  if (!dec.ok) return;
+  u32 tail = commit(d, h, off, seq, n, a.L[li], w, dec, a.ids[r], a.arr[r], now);
+  if (h->err) return;
+  count_stats(h, dec);
+  write_decision(d, s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
+                 a.ratios ? a.ratios + r * G : nullptr);
+  const int g = dec.gpu;
+  if (a.prefill && d.cfg.mode == 0) mark_cached_chain(d, h, tail, g, now);
+  if (h->err) return;
+  if (a.eviction == E2_EVICT_FIFO_TAIL) {
+    if (lane0()) {
+      u64 t = h->fifo_tail[g];
+      u64 i = (u64)g * d.fcap + (t & (d.fcap - 1));
+      if (t - h->fifo_head[g] >= d.fcap) set_err(h, kErrCapacity, kWhyFifoCap);
+      d.fifo_req[i] = r;
+      d.fifo_tail[i] = n - a.trunk;
+      h->fifo_tail[g] = t + 1;
+    }
+    wsync();
+    while (h->cached_tokens[g] > a.hw && h->fifo_head[g] < h->fifo_tail[g] && !h->err) {
+      u64 i = (u64)g * d.fcap + (h->fifo_head[g] & (d.fcap - 1));
+      const i64 k = d.fifo_req[i], tl = d.fifo_tail[i];
+      wsync();
+      if (lane0()) h->fifo_head[g]++;
+      wsync();
+      if (d.cfg.mode == 0) {
+        const i64 kn = a.len[k];
+        uncache_suffix(d, h, d.tok + a.off[k], kn, kn, tl, g);
+      }
+    }
+  } else if (a.eviction == E2_EVICT_MIRROR_LRU) {
+    const i64 cached = h->cached_tokens[g];
+    if (cached > a.hw && d.cfg.mode == 0) evict_lru(d, h, g, cached - a.hw);
+  }
+  if (h->err) return;
+  if (li + a.base >= a.lag) {
+    const i64 k = r - a.lag;
+    note_finished(d, h, a.ids[k], now, a.outl[k]);
+  }
+}
+
+E2_D void serial_body(const Dev& d, Hot* h, Scr* s, const SerialArgs& a) {
+  if (lane0()) h->done = 0;
+  wsync();
+  if (a.kind == 0) {
+    i64 i = 0;
+    for (; i < a.n; ++i) {
+      replay_step(d, h, s, a, i);
+      if (h->err) {
+        if (lane0()) h->err_req = a.base + i;
+        wsync();
+        break;
+      }
+    }
+    if (lane0()) h->done = i;
+    wsync();
+  } else {
+    api_op(d, h, s, a.op, a.out);
+    if (lane0()) h->done = h->err ? 0 : 1;
+    wsync();
+  }
+}
+
+}  // namespace e2

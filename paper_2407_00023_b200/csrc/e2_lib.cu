@@ -1,0 +1,1650 @@
+// e2_lib.cu — the product library: kernels for sm_100a + host orchestration
+// behind the C ABI of include/e2sched.h.
+//
+// Build (see __graft_entry__.build):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared ...
+//        -o paper_2407_00023_b200/libe2sched.so
+// The same file compiled by g++ with -DE2_HOSTSIM (tests/_build only) runs
+// the identical engine on the host with a warp width of 1; that build is a
+// test double for the CPU suite and is never shipped.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "e2_kernels.cuh"
+
+#if E2_DEVICE_BUILD
+#include <cuda_runtime.h>
+#endif
+
+using namespace e2;
+
+// ---------------------------------------------------------------------------
+// memory / launch layer
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Fail : std::runtime_error {
+  int code;
+  Fail(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#if E2_DEVICE_BUILD
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) throw Fail(E2_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+typedef cudaStream_t Stream;
+void* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 8;
+  CK(cudaMalloc(&p, n));
+  CK(cudaMemset(p, 0, n));
+  return p;
+}
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+void h2d(void* dst, const void* src, size_t n, Stream s) {
+  if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s));
+}
+void d2h(void* dst, const void* src, size_t n, Stream s) {
+  if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
+}
+void d2d(void* dst, const void* src, size_t n, Stream s) {
+  if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s));
+}
+void dset(void* p, int v, size_t n, Stream s) {
+  if (n) CK(cudaMemsetAsync(p, v, n, s));
+}
+void ssync(Stream s) { CK(cudaStreamSynchronize(s)); }
+#else
+typedef int Stream;
+void* dalloc(size_t n) {
+  if (n == 0) n = 8;
+  void* p = calloc(1, n);
+  if (!p) throw Fail(E2_ERR_ARG, "host alloc failed");
+  return p;
+}
+void dfree(void* p) { free(p); }
+void h2d(void* dst, const void* src, size_t n, Stream) {
+  if (n) memcpy(dst, src, n);
+}
+void d2h(void* dst, const void* src, size_t n, Stream) {
+  if (n) memcpy(dst, src, n);
+}
+void d2d(void* dst, const void* src, size_t n, Stream) {
+  if (n) memmove(dst, src, n);
+}
+void dset(void* p, int v, size_t n, Stream) {
+  if (n) memset(p, v, n);
+}
+void ssync(Stream) {}
+#endif
+
+template <typename T>
+T* talloc(size_t n) {
+  return (T*)dalloc(n * sizeof(T));
+}
+
+u64 pow2_at_least(u64 v) {
+  u64 p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// grow a device array keeping the first `keep` elements, zero-filling the rest
+template <typename T>
+void grow(T*& p, size_t keep, size_t n, Stream s) {
+  T* q = talloc<T>(n);
+  if (p && keep) d2d(q, p, keep * sizeof(T), s);
+  ssync(s);
+  dfree(p);
+  p = q;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kMatchWarpsPerBlock = 8;
+
+#if E2_DEVICE_BUILD
+__global__ void __launch_bounds__(32, 1) k_serial(Dev d, SerialArgs a) {
+  __shared__ Hot hs;
+  __shared__ Scr ss;
+  {
+    const u64* src = (const u64*)d.hot_g;
+    u64* dst = (u64*)&hs;
+    for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
+  }
+  __syncwarp();
+  serial_body(d, &hs, &ss, a);
+  __syncwarp();
+  {
+    const u64* src = (const u64*)&hs;
+    u64* dst = (u64*)d.hot_g;
+    for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
+  }
+}
+
+__global__ void __launch_bounds__(kMatchWarpsPerBlock * 32) k_match(Dev d, i64 n, i64 base, const i64* off,
+                                                                     const i64* len, i64* S, u32* dslot, u32* dm,
+                                                                     unsigned long long* bytes) {
+  const i64 w = (i64)blockIdx.x * kMatchWarpsPerBlock + (threadIdx.x >> 5);
+  if (w >= n) return;
+  const i64 r = base + w;
+  MatchRes m = match_one(d, d.tok + off[r], len[r]);
+  if (lane0()) {
+    S[w] = m.S;
+    dslot[w] = m.div_slot;
+    dm[w] = m.div_m;
+    atomicAdd(bytes, (unsigned long long)m.bytes);
+  }
+}
+
+__device__ __forceinline__ void gtab_insert(u64* tk, u32* tv, u64 mask, u64 key, u32 i) {
+  u64 idx = key & mask;
+  for (;;) {
+    unsigned long long prev = atomicCAS((unsigned long long*)&tk[idx], 0ull, (unsigned long long)key);
+    if (prev == 0ull || prev == key) {
+      atomicMin(&tv[idx], i);
+      return;
+    }
+    idx = (idx + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ u32 gtab_find(const u64* tk, const u32* tv, u64 mask, u64 key) {
+  u64 idx = key & mask;
+  for (;;) {
+    u64 k = tk[idx];
+    if (k == key) return tv[idx];
+    if (k == 0) return kNil;
+    idx = (idx + 1) & mask;
+  }
+}
+
+__global__ void k_group_init(Dev d, i64 n, i64 base, const i64* off, const i64* len, const i64* S, const u32* dslot,
+                             const u32* dm, i32* state, u64* A, u64* B, i64* cand, i64* L, u64* tk, u32* tv,
+                             u64 mask) {
+  i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const i64 r = base + i;
+  const i64 s = S[i];
+  if (s >= len[r]) {
+    state[i] = 0;
+    L[i] = s;
+    return;
+  }
+  state[i] = 1;
+  A[i] = ((u64)dslot[i] << 32) | (u64)dm[i];
+  B[i] = (u64)(u32)d.tok[off[r] + s];
+  cand[i] = s;
+  gtab_insert(tk, tv, mask, gkey(A[i], B[i], 0), (u32)i);
+}
+
+__global__ void k_group_resolve(i64 n, int round, i32* state, const u64* A, const u64* B, const i64* cand,
+                                i64* leader, i64* o, i64* L, const u64* tk, const u32* tv, u64 mask,
+                                unsigned int* active, unsigned int* collide) {
+  i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || state[i] != 1) return;
+  u32 m = gtab_find(tk, tv, mask, gkey(A[i], B[i], round));
+  if (m == kNil || A[m] != A[i] || B[m] != B[i]) {
+    atomicAdd(collide, 1u);
+    state[i] = 0;
+    L[i] = -1;
+    return;
+  }
+  if ((i64)m == i) {
+    state[i] = 0;
+    L[i] = cand[i];
+  } else {
+    leader[i] = m;
+    o[i] = cand[i] + 1;
+    atomicAdd(active, 1u);
+  }
+}
+
+__global__ void __launch_bounds__(kMatchWarpsPerBlock * 32)
+    k_group_round(Dev d, i64 n, i64 base, int round, const i64* off, const i64* len, i32* state, u64* A, u64* B,
+                  i64* cand, const i64* leader, const i64* o, i64* L, u64* tk, u32* tv, u64 mask,
+                  unsigned long long* bytes) {
+  const i64 i = (i64)blockIdx.x * kMatchWarpsPerBlock + (threadIdx.x >> 5);
+  if (i >= n || state[i] != 1) return;
+  const i64 r = base + i, l = leader[i], rl = base + l;
+  const i64 oi = o[i], ni = len[r], nl = len[rl];
+  const i64 lim = min_(ni, nl) - oi;
+  const i64 a = oi + warp_lcp(d.tok + off[r] + oi, d.tok + off[rl] + oi, lim);
+  if (lane0()) {
+    atomicAdd(bytes, (unsigned long long)(8 * (a - oi + 1)));
+    if (a >= ni) {
+      state[i] = 0;
+      L[i] = a;
+    } else {
+      A[i] = ((u64)l << 32) | (u64)a;
+      B[i] = (u64)(u32)d.tok[off[r] + a];
+      cand[i] = a;
+      gtab_insert(tk, tv, mask, gkey(A[i], B[i], round), (u32)i);
+    }
+  }
+}
+
+__global__ void k_arena_index(i64 n, i64 base_tok, const i64* offsets, i64* off, i64* len, i64 first) {
+  i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  off[first + i] = base_tok + offsets[i] - offsets[0];
+  len[first + i] = offsets[i + 1] - offsets[i];
+}
+#endif
+
+}  // namespace
+
+// last error of calls without a handle (e2_create, e2_generate)
+thread_local std::string g_err;
+void e2_set_global_error(const char* m) { g_err = m; }
+
+// ---------------------------------------------------------------------------
+// handle
+// ---------------------------------------------------------------------------
+struct e2_handle {
+  Dev d;
+  Hot hot;
+  int G = 0;
+  e2_sched_cfg cfg;
+  e2_time_model model;
+  e2_policy pol;
+  Stream stream = 0;
+  bool own_stream = false;
+  // token arena
+  i32* tok = nullptr;
+  i64 tok_len = 0, tok_cap = 0;
+  // per-request arena index for replays / api
+  i64* r_off = nullptr;
+  i64* r_len = nullptr;
+  i64 r_cap = 0;
+  // batch work arrays
+  i64 bcap = 0;
+  i64 *b_S = nullptr, *b_L = nullptr, *b_cand = nullptr, *b_leader = nullptr, *b_o = nullptr;
+  u32 *b_dslot = nullptr, *b_dm = nullptr;
+  i32* b_state = nullptr;
+  u64 *b_A = nullptr, *b_B = nullptr;
+  u64* g_tk = nullptr;
+  u32* g_tv = nullptr;
+  u64 g_mask = 0;
+  unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions
+  unsigned long long* d_bytes = nullptr;  // [0] match bytes, [1] group bytes
+  ApiOut* d_api = nullptr;
+  ApiOut api;
+  // autoscale queue stats (global_scheduler.hpp:157-158): host-side, fed by
+  // note_admitted; prefix root id -> bucket -> (sum, count)
+  std::map<u64, std::map<i64, std::pair<double, i64>>> queue_stats;
+  // profiling
+  bool prof = false;
+  e2_profile acc;
+#if E2_DEVICE_BUILD
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  std::vector<cudaEvent_t> ev_pool;
+#endif
+  std::string err;
+};
+
+namespace {
+
+#if E2_DEVICE_BUILD
+cudaEvent_t ev_get(e2_handle* h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+struct Timed {
+  e2_handle* h;
+  int k;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timed(e2_handle* hh, int kk) : h(hh), k(kk) {
+    h->acc.launches[k]++;
+    if (h->prof) {
+      a = ev_get(h);
+      b = ev_get(h);
+      CK(cudaEventRecord(a, h->stream));
+    }
+  }
+  ~Timed() {
+    if (h->prof) {
+      cudaEventRecord(b, h->stream);
+      h->ev.push_back({k, {a, b}});
+    }
+  }
+};
+void prof_flush(e2_handle* h) {
+  if (h->ev.empty()) return;
+  ssync(h->stream);
+  for (auto& e : h->ev) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+    h->acc.ms[e.first] += ms;
+    h->ev_pool.push_back(e.second.first);
+    h->ev_pool.push_back(e.second.second);
+  }
+  h->ev.clear();
+}
+#else
+struct Timed {
+  Timed(e2_handle* h, int k) { h->acc.launches[k]++; }
+};
+void prof_flush(e2_handle*) {}
+#endif
+
+void push_hot(e2_handle* h) { h2d(h->d.hot_g, &h->hot, sizeof(Hot), h->stream); }
+void pull_hot(e2_handle* h) {
+  d2h(&h->hot, h->d.hot_g, sizeof(Hot), h->stream);
+  ssync(h->stream);
+}
+
+void zero_ptrs(Dev& d) {
+  Cfg c = d.cfg;
+  memset(&d, 0, sizeof(d));
+  d.cfg = c;
+}
+
+// ---- capacity management ---------------------------------------------------
+void host_rehash_ct(e2_handle* h, u64 new_cap) {
+  Dev& d = h->d;
+  const u64 old_cap = d.ct_mask + 1;
+  std::vector<u64> ok(old_cap);
+  std::vector<u32> ov(old_cap);
+  if (d.ck) {
+    d2h(ok.data(), d.ck, old_cap * 8, h->stream);
+    d2h(ov.data(), d.cv, old_cap * 4, h->stream);
+    ssync(h->stream);
+  }
+  std::vector<u64> nk(new_cap, kEmptyKey);
+  std::vector<u32> nv(new_cap, 0);
+  const u64 mask = new_cap - 1;
+  if (d.ck) {
+    for (u64 i = 0; i < old_cap; ++i) {
+      u64 k = ok[i];
+      if (k == kEmptyKey || k == kTombKey) continue;
+      u64 j = mix64(k) & mask;
+      while (nk[j] != kEmptyKey) j = (j + 1) & mask;
+      nk[j] = k;
+      nv[j] = ov[i];
+    }
+  }
+  dfree(d.ck);
+  dfree(d.cv);
+  d.ck = talloc<u64>(new_cap);
+  d.cv = talloc<u32>(new_cap);
+  h2d(d.ck, nk.data(), new_cap * 8, h->stream);
+  h2d(d.cv, nv.data(), new_cap * 4, h->stream);
+  ssync(h->stream);
+  d.ct_mask = mask;
+}
+
+void reserve_nodes(e2_handle* h, u64 need) {
+  Dev& d = h->d;
+  if (need <= d.node_cap && d.hdr) return;
+  const int G = h->G;
+  u64 cap = std::max<u64>(need, (u64)d.node_cap * 2);
+  cap = std::max<u64>(cap, 1024);
+  if (cap > 0xfffffff0ull) throw Fail(E2_ERR_ARG, "node capacity exceeds 32-bit slots");
+  const u64 keep = h->hot.slots_used;
+  grow(d.hdr, keep, cap, h->stream);
+  grow(d.cmask, keep, cap, h->stream);
+  grow(d.lamask, keep, cap, h->stream);
+  grow(d.nchild, keep, cap, h->stream);
+  grow(d.la, keep * G, cap * G, h->stream);
+  grow(d.hits, keep * G, cap * G, h->stream);
+  grow(d.ccc, keep * G, cap * G, h->stream);
+  d.node_cap = (u32)cap;
+  // child table at load <= 1/2
+  u64 ct = pow2_at_least(2 * cap);
+  if (!d.ck || ct > d.ct_mask + 1) host_rehash_ct(h, ct);
+  // LRU pages: each page holds >= 1 key; keys <= cached nodes
+  u64 pages = cap / 2 + 1024 * (u64)G;
+  if (pages > d.page_cap || !d.pg_la) {
+    const u64 kp = h->hot.pages_used;
+    grow(d.pg_la, kp * kPage, pages * kPage, h->stream);
+    grow(d.pg_id, kp * kPage, pages * kPage, h->stream);
+    grow(d.pg_slot, kp * kPage, pages * kPage, h->stream);
+    grow(d.pg_n, kp, pages, h->stream);
+    grow(d.free_pages, h->hot.free_top, pages, h->stream);
+    d.page_cap = (u32)pages;
+  }
+  // directory ring per instance
+  u64 dcap = pow2_at_least(std::max<u64>(cap / 8 + 1024, 1024));
+  if (dcap > d.dcap) {
+    u32* np = talloc<u32>(dcap * G);
+    u64* nla = talloc<u64>(dcap * G);
+    u64* nid = talloc<u64>(dcap * G);
+    if (d.dir_page) {
+      std::vector<u32> op(d.dcap * (u64)G), pp(dcap * G, 0);
+      std::vector<u64> ol(d.dcap * (u64)G), oi(d.dcap * (u64)G), pl(dcap * G, 0), pi(dcap * G, 0);
+      d2h(op.data(), d.dir_page, op.size() * 4, h->stream);
+      d2h(ol.data(), d.dir_la, ol.size() * 8, h->stream);
+      d2h(oi.data(), d.dir_id, oi.size() * 8, h->stream);
+      ssync(h->stream);
+      for (int g = 0; g < G; ++g) {
+        for (u32 k = 0; k < h->hot.dir_n[g]; ++k) {
+          u64 src = (u64)g * d.dcap + ((h->hot.dir_head[g] + k) & (d.dcap - 1));
+          u64 dst = (u64)g * dcap + k;
+          pp[dst] = op[src];
+          pl[dst] = ol[src];
+          pi[dst] = oi[src];
+        }
+        h->hot.dir_head[g] = 0;
+      }
+      h2d(np, pp.data(), pp.size() * 4, h->stream);
+      h2d(nla, pl.data(), pl.size() * 8, h->stream);
+      h2d(nid, pi.data(), pi.size() * 8, h->stream);
+      ssync(h->stream);
+      dfree(d.dir_page);
+      dfree(d.dir_la);
+      dfree(d.dir_id);
+    }
+    d.dir_page = np;
+    d.dir_la = nla;
+    d.dir_id = nid;
+    d.dcap = (u32)dcap;
+    push_hot(h);
+  }
+  // plan scratch
+  if (!d.scr_slot) {
+    d.scap = 1u << 16;
+    d.vcap = 1u << 16;
+    d.scr_slot = talloc<u32>((u64)d.scap * G);
+    d.scr_la = talloc<u64>((u64)d.scap * G);
+    d.scr_id = talloc<u64>((u64)d.scap * G);
+    d.scr_val = talloc<i64>((u64)d.scap * G + 1);
+    d.vic_slot = talloc<u32>(d.vcap);
+    d.vic_tok = talloc<i64>(d.vcap);
+  }
+}
+
+// relayout a monotone-index ring (per instance) into a larger capacity
+template <typename T>
+void ring_regrow(e2_handle* h, T*& arr, u64 oldcap, u64 newcap, const u64* heads, const u64* tails) {
+  const int G = h->G;
+  T* na = talloc<T>(newcap * G);
+  if (arr && oldcap) {
+    std::vector<T> o(oldcap * G), n(newcap * G);
+    d2h(o.data(), arr, o.size() * sizeof(T), h->stream);
+    ssync(h->stream);
+    for (int g = 0; g < G; ++g)
+      for (u64 i = heads[g]; i < tails[g]; ++i) n[(u64)g * newcap + (i & (newcap - 1))] = o[(u64)g * oldcap + (i & (oldcap - 1))];
+    h2d(na, n.data(), n.size() * sizeof(T), h->stream);
+    ssync(h->stream);
+  }
+  dfree(arr);
+  arr = na;
+}
+
+void reserve_window(e2_handle* h, u64 entries) {
+  Dev& d = h->d;
+  u64 cap = pow2_at_least(std::max<u64>(entries, 1024));
+  if (cap <= d.wcap) return;
+  ring_regrow(h, d.ws_t, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
+  ring_regrow(h, d.ws_missed, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
+  ring_regrow(h, d.ws_est, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
+  ring_regrow(h, d.ws_slot, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
+  ring_regrow(h, d.wc_t, d.wcap, cap, h->hot.wc_head, h->hot.wc_tail);
+  ring_regrow(h, d.wc_out, d.wcap, cap, h->hot.wc_head, h->hot.wc_tail);
+  d.wcap = cap;
+}
+
+void reserve_fifo(e2_handle* h, u64 entries) {
+  Dev& d = h->d;
+  u64 cap = pow2_at_least(std::max<u64>(entries, 64));
+  if (cap <= d.fcap) return;
+  ring_regrow(h, d.fifo_req, d.fcap, cap, h->hot.fifo_head, h->hot.fifo_tail);
+  ring_regrow(h, d.fifo_tail, d.fcap, cap, h->hot.fifo_head, h->hot.fifo_tail);
+  d.fcap = cap;
+}
+
+void reserve_inflight(e2_handle* h, u64 live) {
+  Dev& d = h->d;
+  u64 cap = pow2_at_least(std::max<u64>(4 * live + 64, 1024));
+  if (d.inf_key && cap <= d.inf_mask + 1) return;
+  const u64 oc = d.inf_key ? d.inf_mask + 1 : 0;
+  std::vector<i64> ok(oc), oc_(oc), op(oc);
+  std::vector<i32> og(oc);
+  std::vector<double> oa(oc);
+  std::vector<u64> orr(oc);
+  if (oc) {
+    d2h(ok.data(), d.inf_key, oc * 8, h->stream);
+    d2h(og.data(), d.inf_gpu, oc * 4, h->stream);
+    d2h(oc_.data(), d.inf_cached, oc * 8, h->stream);
+    d2h(op.data(), d.inf_prompt, oc * 8, h->stream);
+    d2h(oa.data(), d.inf_arr, oc * 8, h->stream);
+    d2h(orr.data(), d.inf_root, oc * 8, h->stream);
+    ssync(h->stream);
+  }
+  std::vector<i64> nk(cap, kNoInflight), nc(cap, 0), np(cap, 0);
+  std::vector<i32> ng(cap, 0);
+  std::vector<double> na(cap, 0);
+  std::vector<u64> nr(cap, 0);
+  const u64 mask = cap - 1;
+  for (u64 i = 0; i < oc; ++i) {
+    if (ok[i] == kNoInflight) continue;
+    u64 j = mix64((u64)ok[i]) & mask;
+    while (nk[j] != kNoInflight) j = (j + 1) & mask;
+    nk[j] = ok[i];
+    ng[j] = og[i];
+    nc[j] = oc_[i];
+    np[j] = op[i];
+    na[j] = oa[i];
+    nr[j] = orr[i];
+  }
+  dfree(d.inf_key);
+  dfree(d.inf_gpu);
+  dfree(d.inf_cached);
+  dfree(d.inf_prompt);
+  dfree(d.inf_arr);
+  dfree(d.inf_root);
+  d.inf_key = talloc<i64>(cap);
+  d.inf_gpu = talloc<i32>(cap);
+  d.inf_cached = talloc<i64>(cap);
+  d.inf_prompt = talloc<i64>(cap);
+  d.inf_arr = talloc<double>(cap);
+  d.inf_root = talloc<u64>(cap);
+  h2d(d.inf_key, nk.data(), cap * 8, h->stream);
+  h2d(d.inf_gpu, ng.data(), cap * 4, h->stream);
+  h2d(d.inf_cached, nc.data(), cap * 8, h->stream);
+  h2d(d.inf_prompt, np.data(), cap * 8, h->stream);
+  h2d(d.inf_arr, na.data(), cap * 8, h->stream);
+  h2d(d.inf_root, nr.data(), cap * 8, h->stream);
+  ssync(h->stream);
+  d.inf_mask = mask;
+}
+
+void reserve_tokens(e2_handle* h, i64 need) {
+  if (need + 128 <= h->tok_cap) return;
+  i64 cap = std::max<i64>(need + 128, h->tok_cap * 2);
+  cap = std::max<i64>(cap, 1 << 16);
+  grow(h->tok, (size_t)h->tok_len, (size_t)cap, h->stream);
+  h->tok_cap = cap;
+  h->d.tok = h->tok;
+}
+
+void reserve_requests(e2_handle* h, i64 need) {
+  if (need <= h->r_cap) return;
+  i64 cap = std::max<i64>(need, h->r_cap * 2);
+  cap = std::max<i64>(cap, 1024);
+  grow(h->r_off, 0, cap, h->stream);
+  grow(h->r_len, 0, cap, h->stream);
+  h->r_cap = cap;
+}
+
+void reserve_batch(e2_handle* h, i64 B) {
+  if (B <= h->bcap) return;
+  i64 cap = std::max<i64>(B, 256);
+  dfree(h->b_S);
+  dfree(h->b_L);
+  dfree(h->b_cand);
+  dfree(h->b_leader);
+  dfree(h->b_o);
+  dfree(h->b_dslot);
+  dfree(h->b_dm);
+  dfree(h->b_state);
+  dfree(h->b_A);
+  dfree(h->b_B);
+  dfree(h->g_tk);
+  dfree(h->g_tv);
+  h->b_S = talloc<i64>(cap);
+  h->b_L = talloc<i64>(cap);
+  h->b_cand = talloc<i64>(cap);
+  h->b_leader = talloc<i64>(cap);
+  h->b_o = talloc<i64>(cap);
+  h->b_dslot = talloc<u32>(cap);
+  h->b_dm = talloc<u32>(cap);
+  h->b_state = talloc<i32>(cap);
+  h->b_A = talloc<u64>(cap);
+  h->b_B = talloc<u64>(cap);
+  u64 t = pow2_at_least(2 * (u64)cap);
+  h->g_tk = talloc<u64>(t);
+  h->g_tv = talloc<u32>(t);
+  h->g_mask = t - 1;
+  h->bcap = cap;
+}
+
+void check_hot_error(e2_handle* h) {
+  if (h->hot.err == 0) return;
+  static const char* why[] = {"",
+                              "prompt exceeds every GPU's KV capacity",
+                              "global_scheduler: cached spans are not root-contiguous on any GPU",
+                              "prefix_tree: insert of empty sequence",
+                              "prefix_tree: cached_child_count underflow",
+                              "device node pool exhausted",
+                              "device child table full",
+                              "device LRU page pool exhausted",
+                              "device LRU directory exhausted",
+                              "device load window ring exhausted",
+                              "device inflight map exhausted",
+                              "device plan scratch exhausted",
+                              "internal: walk did not find a matched child",
+                              "prefix_tree: split boundary outside edge",
+                              "device FIFO ring exhausted"};
+  int code = h->hot.err;
+  int w = h->hot.why;
+  std::string msg = (w >= 0 && w < (int)(sizeof(why) / sizeof(why[0]))) ? why[w] : "device error";
+  h->hot.err = 0;
+  h->hot.why = 0;
+  push_hot(h);
+  ssync(h->stream);
+  throw Fail(code, msg);
+}
+
+// Ensure capacities for `req` more requests with `toks` more tokens.
+void reserve_for(e2_handle* h, i64 req, i64 toks) {
+  reserve_tokens(h, h->tok_len + toks);
+  reserve_nodes(h, (u64)h->hot.slots_used + 5 * (u64)req + 64);
+  u64 maxw = 0, maxf = 0;
+  for (int g = 0; g < h->G; ++g) {
+    maxw = std::max<u64>(maxw, h->hot.ws_tail[g] - h->hot.ws_head[g]);
+    maxw = std::max<u64>(maxw, h->hot.wc_tail[g] - h->hot.wc_head[g]);
+    maxf = std::max<u64>(maxf, h->hot.fifo_tail[g] - h->hot.fifo_head[g]);
+  }
+  reserve_window(h, maxw + (u64)req + 1);
+  reserve_fifo(h, maxf + (u64)req + 1);
+  reserve_inflight(h, (u64)h->hot.inflight_n + (u64)req + 1);
+}
+
+// ---- launches ---------------------------------------------------------------
+void launch_serial(e2_handle* h, const SerialArgs& a) {
+  {
+    Timed t(h, a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER);
+#if E2_DEVICE_BUILD
+    k_serial<<<1, 32, 0, h->stream>>>(h->d, a);
+    CK(cudaGetLastError());
+#else
+    Scr s;
+    memset(&s, 0, sizeof(s));
+    serial_body(h->d, h->d.hot_g, &s, a);
+#endif
+  }
+}
+
+// K1 + leader rounds for requests [base, base+n) of the arena index.
+// Produces h->b_L[0..n).
+void launch_match(e2_handle* h, i64 base, i64 n) {
+  if (n == 0) return;
+  reserve_batch(h, n);
+  Dev& d = h->d;
+#if E2_DEVICE_BUILD
+  {
+    Timed t(h, E2_K_MATCH);
+    unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
+    k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(d, n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
+                                                             h->b_dm, h->d_bytes);
+    CK(cudaGetLastError());
+  }
+  h->acc.match_requests += n;
+  if (n == 1) {
+    // single sequence: no intra-batch dependency
+    d2d(h->b_L, h->b_S, 8, h->stream);
+    return;
+  }
+  Timed t(h, E2_K_GROUP);
+  const u64 tsz = h->g_mask + 1;
+  const unsigned tg = (unsigned)((n + 255) / 256);
+  dset(h->g_tk, 0, tsz * 8, h->stream);
+  dset(h->g_tv, 0xff, tsz * 4, h->stream);
+  k_group_init<<<tg, 256, 0, h->stream>>>(d, n, base, h->r_off, h->r_len, h->b_S, h->b_dslot, h->b_dm, h->b_state,
+                                          h->b_A, h->b_B, h->b_cand, h->b_L, h->g_tk, h->g_tv, h->g_mask);
+  CK(cudaGetLastError());
+  for (int round = 0;; ++round) {
+    dset(h->d_cnt, 0, 8, h->stream);
+    k_group_resolve<<<tg, 256, 0, h->stream>>>(n, round, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
+                                               h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_cnt, h->d_cnt + 1);
+    CK(cudaGetLastError());
+    unsigned int cnt[2];
+    d2h(cnt, h->d_cnt, 8, h->stream);
+    ssync(h->stream);
+    if (cnt[1]) throw Fail(E2_ERR_ARG, "intra-batch grouping hash collision");
+    if (cnt[0] == 0) break;
+    dset(h->g_tk, 0, tsz * 8, h->stream);
+    dset(h->g_tv, 0xff, tsz * 4, h->stream);
+    unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
+    k_group_round<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(
+        d, n, base, round + 1, h->r_off, h->r_len, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
+        h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_bytes + 1);
+    CK(cudaGetLastError());
+  }
+#else
+  // host emulation: the same per-request functions, sequentially
+  std::vector<i64> S(n);
+  std::vector<u32> ds(n), dm(n);
+  for (i64 w = 0; w < n; ++w) {
+    const i64 r = base + w;
+    MatchRes m = match_one(d, d.tok + h->r_off[r], h->r_len[r]);
+    S[w] = m.S;
+    ds[w] = m.div_slot;
+    dm[w] = m.div_m;
+    h->d_bytes[0] += (unsigned long long)m.bytes;
+  }
+  h->acc.match_requests += n;
+  // leader rounds with std::map grouping (same recursion as the device)
+  std::vector<i32> st(n);
+  std::vector<u64> A(n), B(n);
+  std::vector<i64> cand(n), leader(n), o(n);
+  i64* L = h->b_L;
+  for (i64 i = 0; i < n; ++i) {
+    const i64 r = base + i;
+    if (S[i] >= h->r_len[r]) {
+      st[i] = 0;
+      L[i] = S[i];
+      continue;
+    }
+    st[i] = 1;
+    A[i] = ((u64)ds[i] << 32) | dm[i];
+    B[i] = (u64)(u32)d.tok[h->r_off[r] + S[i]];
+    cand[i] = S[i];
+  }
+  for (int round = 0;; ++round) {
+    std::map<std::pair<u64, u64>, i64> first;
+    for (i64 i = 0; i < n; ++i)
+      if (st[i] == 1) first.emplace(std::make_pair(A[i], B[i]), i);
+    i64 active = 0;
+    for (i64 i = 0; i < n; ++i) {
+      if (st[i] != 1) continue;
+      i64 m = first[std::make_pair(A[i], B[i])];
+      if (m == i) {
+        st[i] = 0;
+        L[i] = cand[i];
+      } else {
+        leader[i] = m;
+        o[i] = cand[i] + 1;
+        active++;
+      }
+    }
+    if (!active) break;
+    for (i64 i = 0; i < n; ++i) {
+      if (st[i] != 1) continue;
+      const i64 r = base + i, rl = base + leader[i];
+      const i64 lim = std::min(h->r_len[r], h->r_len[rl]) - o[i];
+      const i64 a = o[i] + warp_lcp(d.tok + h->r_off[r] + o[i], d.tok + h->r_off[rl] + o[i], lim);
+      if (a >= h->r_len[r]) {
+        st[i] = 0;
+        L[i] = a;
+      } else {
+        A[i] = ((u64)leader[i] << 32) | (u64)a;
+        B[i] = (u64)(u32)d.tok[h->r_off[r] + a];
+        cand[i] = a;
+      }
+    }
+  }
+#endif
+}
+
+// Append sequences to the arena and index them at request slots [first, first+n).
+void append_host_seq(e2_handle* h, const i32* seq, i64 len, i64 slot) {
+  reserve_tokens(h, h->tok_len + len);
+  reserve_requests(h, slot + 1);
+  h2d(h->tok + h->tok_len, seq, (size_t)len * 4, h->stream);
+  i64 o = h->tok_len, l = len;
+  h2d(h->r_off + slot, &o, 8, h->stream);
+  h2d(h->r_len + slot, &l, 8, h->stream);
+  h->tok_len += len;
+}
+
+// One API op on one sequence (or none): append, match, run.
+void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match) {
+  reserve_for(h, 1, len);
+  if (seq) {
+    append_host_seq(h, seq, len, 0);
+    op.off = h->tok_len - len;
+    op.len = len;
+    if (need_match) {
+      launch_match(h, 0, 1);
+      i64 L = 0;
+      d2h(&L, h->b_L, 8, h->stream);
+      ssync(h->stream);
+      op.L = L;
+    }
+  }
+  SerialArgs a;
+  memset(&a, 0, sizeof(a));
+  a.kind = 1;
+  a.op = op;
+  a.out = h->d_api;
+  push_hot(h);
+  launch_serial(h, a);
+  pull_hot(h);
+  d2h(&h->api, h->d_api, sizeof(ApiOut), h->stream);
+  ssync(h->stream);
+  check_hot_error(h);
+}
+
+template <typename F>
+int guard(e2_handle* h, F&& f) {
+  try {
+    f();
+    return E2_OK;
+  } catch (const Fail& e) {
+    if (h) h->err = e.what();
+    else g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (h) h->err = e.what();
+    else g_err = e.what();
+    return E2_ERR_ARG;
+  }
+}
+
+bool bad_gpu(e2_handle* h, int32_t g) {
+  if (g < 0 || g >= h->G) {
+    h->err = "gpu id out of range";
+    return true;
+  }
+  return false;
+}
+
+void copy_decision(e2_handle* h, e2_decision* out, e2_cost* costs, double* ratios) {
+  if (out) *out = h->api.dec;
+  if (costs)
+    for (int i = 0; i < h->api.dec.n_costs; ++i) costs[i] = h->api.costs[i];
+  if (ratios && h->api.dec.has_ratios)
+    for (int g = 0; g < h->G; ++g) ratios[g] = h->api.ratios[g];
+}
+
+// ---- autoscale (global_scheduler.cpp:236-338), host-orchestrated --------------
+// Out of the hot path: it only fires after note_admitted fills the
+// queue statistics, which the trace driver never does.
+struct HostTree {
+  std::vector<NodeHdr> hdr;
+  std::vector<u64> cmask, lamask;
+  std::vector<double> la;
+  std::vector<i32> hits;
+  std::vector<std::vector<u32>> kids;  // sorted by first token
+  std::vector<i32> tok;
+};
+
+void pull_tree(e2_handle* h, HostTree& t) {
+  const u64 n = h->hot.slots_used;
+  const int G = h->G;
+  t.hdr.resize(n);
+  t.cmask.resize(n);
+  t.lamask.resize(n);
+  t.la.resize(n * G);
+  t.hits.resize(n * G);
+  d2h(t.hdr.data(), h->d.hdr, n * sizeof(NodeHdr), h->stream);
+  d2h(t.cmask.data(), h->d.cmask, n * 8, h->stream);
+  d2h(t.lamask.data(), h->d.lamask, n * 8, h->stream);
+  d2h(t.la.data(), h->d.la, n * G * 8, h->stream);
+  d2h(t.hits.data(), h->d.hits, n * G * 4, h->stream);
+  t.tok.resize(h->tok_len);
+  d2h(t.tok.data(), h->tok, h->tok_len * 4, h->stream);
+  ssync(h->stream);
+  t.kids.assign(n, {});
+  for (u64 s = 1; s < n; ++s) {
+    if (t.hdr[s].edge_len == 0) continue;
+    t.kids[t.hdr[s].parent].push_back((u32)s);
+  }
+  for (auto& k : t.kids)
+    std::sort(k.begin(), k.end(), [&](u32 a, u32 b) { return t.hdr[a].first_tok < t.hdr[b].first_tok; });
+}
+
+double host_load(e2_handle* h, int g, double now) {
+  OpDesc op;
+  memset(&op, 0, sizeof(op));
+  op.kind = OP_GPU_LOAD;
+  op.gpu = g;
+  op.now = now;
+  run_api(h, op, nullptr, 0, false);
+  return h->api.v;
+}
+
+void run_simple(e2_handle* h, i32 kind, int gpu, i64 x, double now) {
+  OpDesc op;
+  memset(&op, 0, sizeof(op));
+  op.kind = kind;
+  op.gpu = gpu;
+  op.x = x;
+  op.now = now;
+  run_api(h, op, nullptr, 0, false);
+}
+
+double host_prefill_time(const e2_time_model& m, i64 missed) {
+  if (missed <= 0) return 0.0;
+  volatile double a = m.prefill_per_token_ms * (double)missed;
+  volatile double b = m.prefill_base_ms + a;
+  return b;
+}
+
+void replicate_prefix(e2_handle* h, u32 root_child, int target, double now) {
+  run_simple(h, OP_MARK_NODE, target, root_child, now);
+  run_simple(h, OP_EXPIRE_ALL, 0, 0, now);  // windowed hits for all instances
+  HostTree t;
+  pull_tree(h, t);
+  const int G = h->G;
+  struct Kid {
+    u32 node;
+    double load;
+  };
+  std::vector<Kid> kids;
+  for (u32 ch : t.kids[root_child]) {
+    i64 toks = 0;
+    std::vector<u32> st{ch};
+    while (!st.empty()) {
+      u32 x = st.back();
+      st.pop_back();
+      toks += t.hdr[x].edge_len;
+      for (u32 y : t.kids[x]) st.push_back(y);
+    }
+    i64 hits = 0;
+    for (int g = 0; g < G; ++g) hits += t.hits[(u64)ch * G + g];
+    volatile double ld = (double)hits * host_prefill_time(h->model, toks);
+    kids.push_back({ch, ld});
+  }
+  std::sort(kids.begin(), kids.end(), [&](const Kid& a, const Kid& b) {
+    if (a.load != b.load) return a.load > b.load;
+    return t.hdr[a.node].id < t.hdr[b.node].id;
+  });
+  double stay = 0, move = 0;
+  std::vector<u32> moving;
+  for (auto& k : kids) {
+    if (move < stay) {
+      moving.push_back(k.node);
+      move += k.load;
+    } else {
+      stay += k.load;
+    }
+  }
+  for (u32 n : moving) {
+    u64 owners = 0;
+    std::vector<u32> st{n};
+    while (!st.empty()) {
+      u32 x = st.back();
+      st.pop_back();
+      owners |= t.cmask[x];
+      for (u32 y : t.kids[x]) st.push_back(y);
+    }
+    run_simple(h, OP_MARK_SUBTREE, target, n, now);
+    for (int g = 0; g < G; ++g)
+      if (((owners >> g) & 1ull) && g != target) run_simple(h, OP_UNCACHE_SUBTREE, g, n, now);
+  }
+}
+
+void check_autoscale(e2_handle* h, double now) {
+  if (h->queue_stats.empty()) return;
+  const double H = h->cfg.history_window_ms;
+  const i64 cur = (i64)std::floor(now / H);
+  for (auto it = h->queue_stats.begin(); it != h->queue_stats.end();) {
+    auto& buckets = it->second;
+    while (!buckets.empty() && buckets.begin()->first < cur - 1) buckets.erase(buckets.begin());
+    if (buckets.empty()) {
+      it = h->queue_stats.erase(it);
+      continue;
+    }
+    bool fired = false;
+    auto pi = buckets.find(cur - 1);
+    auto ci = buckets.find(cur);
+    if (pi != buckets.end() && ci != buckets.end() && pi->second.second > 0 && ci->second.second > 0) {
+      const double pm = pi->second.first / (double)pi->second.second;
+      const double cm = ci->second.first / (double)ci->second.second;
+      if (pm > 0 && cm >= 2.0 * pm) {
+        HostTree t;
+        pull_tree(h, t);
+        u32 rc = kNil;
+        for (u32 ch : t.kids[kRoot])
+          if (t.hdr[ch].id == it->first) rc = ch;
+        int src = -1;
+        if (rc != kNil) {
+          for (int s = 0; s < h->G; ++s)
+            if (h->hot.redirect[s] >= 0 && ((t.cmask[rc] >> s) & 1ull)) {
+              src = s;
+              break;
+            }
+        }
+        if (src >= 0) {
+          int target = -1;
+          double tl = 0;
+          for (int g = 0; g < h->G; ++g) {
+            if ((t.cmask[rc] >> g) & 1ull) continue;
+            double l = host_load(h, g, now);
+            if (target < 0 || l < tl) {
+              target = g;
+              tl = l;
+            }
+          }
+          if (target >= 0) {
+            replicate_prefix(h, rc, target, now);
+            h->hot.stats[kStAutoscale]++;
+            push_hot(h);
+            fired = true;
+          }
+        }
+      }
+    }
+    if (fired)
+      it = h->queue_stats.erase(it);
+    else
+      ++it;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* e2_backend(void) {
+#if E2_DEVICE_BUILD
+  return "b200";
+#else
+  return "hostsim";
+#endif
+}
+
+int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* model, const e2_policy* policy,
+              e2_handle** out) {
+  *out = nullptr;
+  // ConfigError checks — global_scheduler.cpp:8-15, 27-37
+  if (n_gpus < 1) {
+    g_err = "cluster needs at least one GPU";
+    return E2_ERR_CONFIG;
+  }
+  if (!(cfg->history_window_ms > 0)) {
+    g_err = "history_window_ms must be > 0";
+    return E2_ERR_CONFIG;
+  }
+  if (!(cfg->th_bal > 1.0)) {
+    g_err = "th_bal must be > 1";
+    return E2_ERR_CONFIG;
+  }
+  if (!(cfg->imbal_ratio > 0.0 && cfg->imbal_ratio <= 1.0)) {
+    g_err = "imbal_ratio must be in (0,1]";
+    return E2_ERR_CONFIG;
+  }
+  if (cfg->priority_groups < 1) {
+    g_err = "priority_groups must be >= 1";
+    return E2_ERR_CONFIG;
+  }
+  if (cfg->kv_capacity_tokens <= 0) {
+    g_err = "kv_capacity_tokens must be > 0";
+    return E2_ERR_CONFIG;
+  }
+  if (cfg->default_output_len < 0) {
+    g_err = "default_output_len must be >= 0";
+    return E2_ERR_CONFIG;
+  }
+  if (n_gpus > E2_MAX_GPUS) {
+    g_err = "this implementation supports at most 64 instances";
+    return E2_ERR_ARG;
+  }
+  e2_handle* h = new e2_handle();
+  int rc = guard(nullptr, [&] {
+    h->G = n_gpus;
+    h->cfg = *cfg;
+    h->model = *model;
+    h->pol = *policy;
+    memset(&h->hot, 0, sizeof(h->hot));
+    memset(&h->acc, 0, sizeof(h->acc));
+    for (int g = 0; g < kMaxG; ++g) h->hot.redirect[g] = -1;
+    h->hot.next_id = 1;  // root holds id 0 (prefix_tree.cpp:9-12)
+    h->hot.slots_used = 1;
+    Cfg c;
+    memset(&c, 0, sizeof(c));
+    c.G = n_gpus;
+    c.mode = policy->mode == E2_MODE_ROUND_ROBIN ? 1 : 0;
+    c.rebalance = policy->rebalance;
+    c.autoscale = policy->autoscale;
+    c.pd_balance = policy->pd_balance;
+    c.H = cfg->history_window_ms;
+    c.th_bal = cfg->th_bal;
+    c.imbal = cfg->imbal_ratio;
+    c.cap = cfg->kv_capacity_tokens;
+    c.default_out = cfg->default_output_len;
+    c.c0 = model->prefill_base_ms;
+    c.c1 = model->prefill_per_token_ms;
+    c.c2 = model->decode_per_token_ms;
+    c.c3 = model->iteration_base_ms;
+    zero_ptrs(h->d);
+    h->d.cfg = c;
+#if E2_DEVICE_BUILD
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+#endif
+    h->d.hot_g = talloc<Hot>(1);
+    h->d_api = talloc<ApiOut>(1);
+    h->d_cnt = talloc<unsigned int>(2);
+    h->d_bytes = talloc<unsigned long long>(2);
+    reserve_nodes(h, 1024);
+    reserve_window(h, 1024);
+    reserve_fifo(h, 64);
+    reserve_inflight(h, 64);
+    reserve_tokens(h, 1 << 16);
+    reserve_requests(h, 1024);
+    // root node: slot 0, id 0
+    NodeHdr root;
+    memset(&root, 0, sizeof(root));
+    root.parent = kNil;
+    h2d(h->d.hdr, &root, sizeof(root), h->stream);
+    push_hot(h);
+    ssync(h->stream);
+  });
+  if (rc != E2_OK) {
+    if (g_err.empty()) g_err = h->err;
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return E2_OK;
+}
+
+void e2_destroy(e2_handle* h) {
+  if (!h) return;
+  Dev& d = h->d;
+  void* ptrs[] = {d.hdr, d.cmask, d.lamask, d.nchild, d.la, d.hits, d.ccc, d.ck, d.cv, d.ws_t, d.ws_missed, d.ws_est,
+                  d.ws_slot, d.wc_t, d.wc_out, d.dir_page, d.dir_la, d.dir_id, d.pg_la, d.pg_id, d.pg_slot, d.pg_n,
+                  d.free_pages, d.inf_key, d.inf_gpu, d.inf_cached, d.inf_prompt, d.inf_arr, d.inf_root, d.fifo_req,
+                  d.fifo_tail, d.scr_slot, d.scr_val, d.scr_la, d.scr_id, d.vic_slot, d.vic_tok, d.hot_g, h->tok,
+                  h->r_off, h->r_len, h->b_S, h->b_L, h->b_cand, h->b_leader, h->b_o, h->b_dslot, h->b_dm,
+                  h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api};
+  for (void* p : ptrs) dfree(p);
+#if E2_DEVICE_BUILD
+  for (auto& e : h->ev) {
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+#endif
+  delete h;
+}
+
+const char* e2_last_error(const e2_handle* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int e2_schedule(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t request_id, double arrival_ms,
+                double now, e2_decision* out, e2_cost* costs, double* ratios) {
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_SCHEDULE;
+    op.id = request_id;
+    op.arr = arrival_ms;
+    op.now = now;
+    static const i32 dummy = 0;
+    run_api(h, op, prompt_len ? prompt : &dummy, prompt_len, true);
+    copy_decision(h, out, costs, ratios);
+    if (h->pol.mode == E2_MODE_PREFIX_AWARE && h->pol.autoscale) check_autoscale(h, now);
+  });
+}
+
+int e2_decide(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t request_id, double now,
+              e2_decision* out, e2_cost* costs, double* ratios) {
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_DECIDE;
+    op.id = request_id;
+    op.now = now;
+    static const i32 dummy = 0;
+    run_api(h, op, prompt_len ? prompt : &dummy, prompt_len, true);
+    copy_decision(h, out, costs, ratios);
+  });
+}
+
+int e2_note_admitted(e2_handle* h, int64_t request_id, double now) {
+  return guard(h, [&] {
+    if (h->pol.mode != E2_MODE_PREFIX_AWARE) return;
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_INFLIGHT_GET;
+    op.id = request_id;
+    run_api(h, op, nullptr, 0, false);
+    if (!h->api.i0) return;
+    const i64 bucket = (i64)std::floor(now / h->cfg.history_window_ms);
+    auto& cell = h->queue_stats[h->api.u0][bucket];
+    cell.first += now - h->api.v;
+    cell.second += 1;
+  });
+}
+
+int e2_note_prefill_cached(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int32_t gpu, double now) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    if (h->pol.mode != E2_MODE_PREFIX_AWARE || prompt_len == 0) return;
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_PREFILL;
+    op.gpu = gpu;
+    op.now = now;
+    run_api(h, op, prompt, prompt_len, true);
+  });
+}
+
+int e2_note_eviction(e2_handle* h, const int32_t* seq, int64_t seq_len, int64_t tail_len, int32_t gpu, double now) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    if (h->pol.mode != E2_MODE_PREFIX_AWARE || seq_len == 0 || tail_len <= 0) return;
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_EVICT;
+    op.gpu = gpu;
+    op.x = tail_len;
+    op.now = now;
+    run_api(h, op, seq, seq_len, true);
+  });
+}
+
+int e2_note_finished(e2_handle* h, int64_t request_id, double now, int64_t output_len) {
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_FINISHED;
+    op.id = request_id;
+    op.now = now;
+    op.x = output_len;
+    run_api(h, op, nullptr, 0, false);
+  });
+}
+
+int e2_decode_ratio(e2_handle* h, int32_t gpu, double* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    pull_hot(h);
+    const i64 ip = h->hot.inflight_prompt[gpu];
+    *out = ip <= 0 ? 0.0 : (double)h->hot.inflight_cached[gpu] / (double)ip;
+  });
+}
+
+int e2_gpu_load_ms(e2_handle* h, int32_t gpu, double now, double* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] { *out = host_load(h, gpu, now); });
+}
+
+int e2_prune_dead_nodes(e2_handle* h, double now, int64_t* removed) {
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_PRUNE_DEAD;
+    op.now = now;
+    run_api(h, op, nullptr, 0, false);
+    *removed = h->api.i0;
+  });
+}
+
+int e2_cached_tokens(e2_handle* h, int32_t gpu, int64_t* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    pull_hot(h);
+    *out = h->hot.cached_tokens[gpu];
+  });
+}
+
+int e2_node_count(e2_handle* h, int64_t* out) {
+  return guard(h, [&] {
+    pull_hot(h);
+    *out = h->hot.node_count;
+  });
+}
+
+int e2_redirects(e2_handle* h, int32_t* out) {
+  return guard(h, [&] {
+    pull_hot(h);
+    for (int g = 0; g < h->G; ++g) out[g] = h->hot.redirect[g];
+  });
+}
+
+int e2_get_stats(e2_handle* h, e2_stats* out) {
+  return guard(h, [&] {
+    pull_hot(h);
+    out->exploit = h->hot.stats[kStExploit];
+    out->explore = h->hot.stats[kStExplore];
+    out->decode_pressure = h->hot.stats[kStPressure];
+    out->round_robin = h->hot.stats[kStRoundRobin];
+    out->redirected = h->hot.stats[kStRedirected];
+    out->rebalance_installs = h->hot.stats[kStInstalls];
+    out->autoscale_events = h->hot.stats[kStAutoscale];
+    out->tree_reads = h->hot.stats[kStTreeReads];
+  });
+}
+
+int e2_load_cost(e2_handle* h, int32_t gpu, int64_t missed_tokens, double now, e2_cost* out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_LOAD_COST;
+    op.gpu = gpu;
+    op.x = missed_tokens;
+    op.now = now;
+    run_api(h, op, nullptr, 0, false);
+    *out = h->api.costs[0];
+  });
+}
+
+int e2_match(e2_handle* h, const int32_t* seq, int64_t len, int64_t* matched_len, int64_t* cached_len,
+             int64_t* per_gpu) {
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_MATCH;
+    static const i32 dummy = 0;
+    run_api(h, op, len ? seq : &dummy, len, true);
+    if (matched_len) *matched_len = h->api.i0;
+    if (cached_len) *cached_len = h->api.i1;
+    if (per_gpu)
+      for (int g = 0; g < h->G; ++g) per_gpu[g] = h->api.ext[g];
+  });
+}
+
+int e2_window_sizes(e2_handle* h, int32_t gpu, double now, int64_t* n_scheduled, int64_t* n_completed,
+                    int64_t* inflight_cached, int64_t* inflight_prompt) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_WINDOW;
+    op.gpu = gpu;
+    op.now = now;
+    run_api(h, op, nullptr, 0, false);
+    if (n_scheduled) *n_scheduled = h->api.i0;
+    if (n_completed) *n_completed = h->api.i1;
+    if (inflight_cached) *inflight_cached = h->api.i2;
+    if (inflight_prompt) *inflight_prompt = h->api.i3;
+  });
+}
+
+// ---- export / dump (host-side; off the hot path) ---------------------------
+namespace {
+void expire_all(e2_handle* h, double now) { run_simple(h, OP_EXPIRE_ALL, 0, 0, now); }
+
+void dfs_order(const HostTree& t, std::vector<std::pair<u32, int>>& order) {
+  std::vector<std::pair<u32, int>> st{{kRoot, 0}};
+  while (!st.empty()) {
+    auto [x, dep] = st.back();
+    st.pop_back();
+    order.push_back({x, dep});
+    const auto& k = t.kids[x];
+    for (size_t i = k.size(); i-- > 0;) st.push_back({k[i], dep + 1});
+  }
+}
+}  // namespace
+
+int e2_export_size(e2_handle* h, int64_t* n_nodes, int64_t* n_tokens) {
+  return guard(h, [&] {
+    HostTree t;
+    pull_tree(h, t);
+    std::vector<std::pair<u32, int>> order;
+    dfs_order(t, order);
+    i64 nt = 0;
+    for (auto& [x, dep] : order) nt += t.hdr[x].edge_len;
+    *n_nodes = (i64)order.size();
+    *n_tokens = nt;
+  });
+}
+
+int e2_export(e2_handle* h, double now, e2_node* nodes, int32_t* tokens, double* last_access, int64_t* hits) {
+  return guard(h, [&] {
+    expire_all(h, now);
+    HostTree t;
+    pull_tree(h, t);
+    std::vector<std::pair<u32, int>> order;
+    dfs_order(t, order);
+    const int G = h->G;
+    i64 off = 0;
+    for (size_t i = 0; i < order.size(); ++i) {
+      const u32 x = order[i].first;
+      const NodeHdr& hd = t.hdr[x];
+      if (nodes) {
+        nodes[i].id = hd.id;
+        nodes[i].parent_id = x == kRoot ? hd.id : t.hdr[hd.parent].id;
+        nodes[i].edge_off = off;
+        nodes[i].edge_len = hd.edge_len;
+        nodes[i].caching_mask = t.cmask[x];
+        nodes[i].last_access_mask = t.lamask[x];
+        nodes[i].pin_count = 0;
+      }
+      if (tokens && hd.edge_len) memcpy(tokens + off, t.tok.data() + hd.edge_off, (size_t)hd.edge_len * 4);
+      off += hd.edge_len;
+      for (int g = 0; g < G; ++g) {
+        if (last_access) last_access[i * G + g] = ((t.lamask[x] >> g) & 1ull) ? t.la[(u64)x * G + g] : 0.0;
+        if (hits) hits[i * G + g] = t.hits[(u64)x * G + g];
+      }
+    }
+  });
+}
+
+int e2_debug_dump(e2_handle* h, double now, char* buf, size_t cap, size_t* needed) {
+  return guard(h, [&] {
+    expire_all(h, now);
+    HostTree t;
+    pull_tree(h, t);
+    std::vector<std::pair<u32, int>> order;
+    dfs_order(t, order);
+    std::string s;
+    const int G = h->G;
+    char tmp[64];
+    for (auto& [x, dep] : order) {
+      for (int i = 0; i < dep; ++i) s += "  ";
+      snprintf(tmp, sizeof(tmp), "d%d len=%u gpus=[", dep, t.hdr[x].edge_len);
+      s += tmp;
+      bool first = true;
+      for (int g = 0; g < G; ++g)
+        if ((t.cmask[x] >> g) & 1ull) {
+          if (!first) s += ",";
+          s += std::to_string(g);
+          first = false;
+        }
+      s += "] hits=[";
+      first = true;
+      for (int g = 0; g < G; ++g) {
+        i32 c = t.hits[(u64)x * G + g];
+        if (c == 0) continue;
+        if (!first) s += ",";
+        s += std::to_string(g) + ":" + std::to_string(c);
+        first = false;
+      }
+      s += "]\n";
+    }
+    if (needed) *needed = s.size();
+    if (buf && cap > 0) {
+      size_t k = std::min(cap - 1, s.size());
+      memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
+  });
+}
+
+// ---- batched replay ---------------------------------------------------------
+namespace {
+int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const int64_t* ids,
+                const double* arrivals, const int64_t* output_lens, int64_t n, const e2_driver_cfg* drv,
+                e2_decision* out, e2_cost* costs, double* ratios, int64_t* n_done, bool device_ptrs) {
+  if (n_done) *n_done = 0;
+  return guard(h, [&] {
+    if (n <= 0) return;
+    if (!h->queue_stats.empty() && h->pol.autoscale && h->pol.mode == E2_MODE_PREFIX_AWARE)
+      throw Fail(E2_ERR_ARG, "replay with pending autoscale queue statistics is not supported");
+    const int G = h->G;
+    i64 off0 = 0, offn = 0;
+    if (device_ptrs) {
+      d2h(&off0, offsets, 8, h->stream);
+      d2h(&offn, offsets + n, 8, h->stream);
+      ssync(h->stream);
+    } else {
+      off0 = offsets[0];
+      offn = offsets[n];
+    }
+    const i64 ntok = offn - off0;
+    reserve_for(h, n, ntok);
+    reserve_requests(h, n);
+    // token arena: append the trace
+    const i64 base_tok = h->tok_len;
+    const i64 pad = (4 - (base_tok & 3)) & 3;  // 16-byte align the trace start
+    reserve_tokens(h, base_tok + pad + ntok);
+    const i64 tstart = base_tok + pad;
+    if (device_ptrs)
+      d2d(h->tok + tstart, tokens + off0, (size_t)ntok * 4, h->stream);
+    else
+      h2d(h->tok + tstart, tokens + off0, (size_t)ntok * 4, h->stream);
+    h->tok_len = tstart + ntok;
+    // per-request arrays resident on the device
+    i64 *d_ids = nullptr, *d_out = nullptr, *d_offs = nullptr;
+    double* d_arr = nullptr;
+    e2_decision* d_dec = nullptr;
+    e2_cost* d_cost = nullptr;
+    double* d_rat = nullptr;
+    std::vector<void*> owned;
+    if (device_ptrs) {
+      d_ids = (i64*)ids;
+      d_arr = (double*)arrivals;
+      d_out = (i64*)output_lens;
+      d_offs = (i64*)offsets;
+      d_dec = out;
+      d_cost = costs;
+      d_rat = ratios;
+    } else {
+      d_ids = talloc<i64>(n);
+      d_arr = talloc<double>(n);
+      d_out = talloc<i64>(n);
+      d_offs = talloc<i64>(n + 1);
+      d_dec = talloc<e2_decision>(n);
+      owned = {d_ids, d_arr, d_out, d_offs, d_dec};
+      if (costs) {
+        d_cost = talloc<e2_cost>((size_t)n * (G + 1));
+        owned.push_back(d_cost);
+      }
+      if (ratios) {
+        d_rat = talloc<double>((size_t)n * G);
+        owned.push_back(d_rat);
+      }
+      h2d(d_ids, ids, n * 8, h->stream);
+      h2d(d_arr, arrivals, n * 8, h->stream);
+      h2d(d_out, output_lens, n * 8, h->stream);
+      h2d(d_offs, offsets, (n + 1) * 8, h->stream);
+    }
+#if E2_DEVICE_BUILD
+    {
+      Timed t(h, E2_K_OTHER);
+      k_arena_index<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(n, tstart, d_offs, h->r_off, h->r_len, 0);
+      CK(cudaGetLastError());
+    }
+#else
+    for (i64 i = 0; i < n; ++i) {
+      h->r_off[i] = tstart + d_offs[i] - d_offs[0];
+      h->r_len[i] = d_offs[i + 1] - d_offs[i];
+    }
+#endif
+    // driver state
+    h->hot.drv_now = 0;
+    for (int g = 0; g < G; ++g) h->hot.fifo_head[g] = h->hot.fifo_tail[g] = 0;
+    push_hot(h);
+    const i64 B = drv->batch > 0 ? drv->batch : 16384;
+    reserve_batch(h, std::min<i64>(B, n));
+    SerialArgs a;
+    memset(&a, 0, sizeof(a));
+    a.kind = 0;
+    a.eviction = drv->eviction;
+    a.prefill = drv->prefill_cached;
+    a.off = h->r_off;
+    a.len = h->r_len;
+    a.ids = d_ids;
+    a.arr = d_arr;
+    a.outl = d_out;
+    a.L = h->b_L;
+    a.dec = d_dec;
+    a.costs = d_cost;
+    a.ratios = d_rat;
+    a.trunk = drv->trunk_len;
+    a.hw = drv->high_water;
+    a.lag = drv->finish_lag;
+    i64 done = 0;
+    std::string fail;
+    int fail_code = 0;
+    for (i64 b0 = 0; b0 < n; b0 += B) {
+      const i64 nb = std::min<i64>(B, n - b0);
+      launch_match(h, b0, nb);
+      a.base = b0;
+      a.n = nb;
+      launch_serial(h, a);
+      pull_hot(h);
+      done = b0 + h->hot.done;
+      if (h->hot.err) {
+        try {
+          check_hot_error(h);
+        } catch (const Fail& e) {
+          fail = e.what();
+          fail_code = e.code;
+        }
+        break;
+      }
+    }
+    prof_flush(h);
+    if (!device_ptrs) {
+      d2h(out, d_dec, (size_t)done * sizeof(e2_decision), h->stream);
+      if (costs) d2h(costs, d_cost, (size_t)done * (G + 1) * sizeof(e2_cost), h->stream);
+      if (ratios) d2h(ratios, d_rat, (size_t)done * G * 8, h->stream);
+      ssync(h->stream);
+      for (void* p : owned) dfree(p);
+    }
+    if (n_done) *n_done = done;
+    if (fail_code) throw Fail(fail_code, fail + " (request index " + std::to_string(done) + ")");
+  });
+}
+}  // namespace
+
+int e2_replay(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const int64_t* ids, const double* arrivals,
+              const int64_t* output_lens, int64_t n, const e2_driver_cfg* drv, e2_decision* out, e2_cost* costs,
+              double* ratios, int64_t* n_done) {
+  return replay_impl(h, tokens, offsets, ids, arrivals, output_lens, n, drv, out, costs, ratios, n_done, false);
+}
+
+int e2_replay_device(e2_handle* h, const int32_t* d_tokens, const int64_t* d_offsets, const int64_t* d_ids,
+                     const double* d_arrivals, const int64_t* d_output_lens, int64_t n, const e2_driver_cfg* drv,
+                     e2_decision* d_out, e2_cost* d_costs, double* d_ratios, void* stream, int64_t* n_done) {
+#if E2_DEVICE_BUILD
+  Stream saved = h->stream;
+  if (stream) h->stream = (Stream)stream;
+  int rc = replay_impl(h, d_tokens, d_offsets, d_ids, d_arrivals, d_output_lens, n, drv, d_out, d_costs, d_ratios,
+                       n_done, true);
+  h->stream = saved;
+  return rc;
+#else
+  (void)stream;
+  return replay_impl(h, d_tokens, d_offsets, d_ids, d_arrivals, d_output_lens, n, drv, d_out, d_costs, d_ratios,
+                     n_done, true);
+#endif
+}
+
+int e2_profile_get(e2_handle* h, e2_profile* out) {
+  return guard(h, [&] {
+    prof_flush(h);
+    unsigned long long b[2] = {0, 0};
+    d2h(b, h->d_bytes, 16, h->stream);
+    ssync(h->stream);
+    *out = h->acc;
+    out->match_bytes = (i64)b[0];
+  });
+}
+
+int e2_profile_reset(e2_handle* h, int32_t enable_timing) {
+  return guard(h, [&] {
+    prof_flush(h);
+    memset(&h->acc, 0, sizeof(h->acc));
+    h->prof = enable_timing != 0;
+    dset(h->d_bytes, 0, 16, h->stream);
+    ssync(h->stream);
+  });
+}
+
+}  // extern "C"

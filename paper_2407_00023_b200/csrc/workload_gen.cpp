@@ -1,0 +1,305 @@
+// workload_gen.cpp — synthetic trace generation (input only, host C++).
+//
+// For the reference archetypes the RNG draw sequence is the one of
+// kvsched::generate / assign_poisson_arrivals (proj/src/workload.cpp:235-327,
+// 486-497): mt19937_64 with libstdc++'s distributions in the same order, and
+// the same disjoint token-id regions (workload.cpp:25-28), so traces are
+// bit-identical (pinned by tests/test_workload.py against the reference).
+// Extensions for SURVEY 8(d): per-trunk length ranges for config 3
+// (branch_len_max > branch_len) and a tree-of-thought archetype for config 4.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "e2sched.h"
+
+namespace {
+
+constexpr int64_t kSys = 1000000;
+constexpr int64_t kTrunk = 2000000;
+constexpr int64_t kFresh = 500000000;
+constexpr int64_t kIdMax = 2147483647;
+
+struct Builder {
+  std::vector<int32_t> tok;
+  std::vector<int64_t> off{0};
+  std::vector<int64_t> out;
+  int64_t fresh = kFresh;
+
+  void fresh_ids(std::vector<int32_t>& v, int64_t n) {
+    if (fresh + n > kIdMax) throw std::runtime_error("workload: token id space exhausted");
+    for (int64_t i = 0; i < n; ++i) v.push_back((int32_t)(fresh++));
+  }
+  void emit(const std::vector<int32_t>& p, int64_t o) {
+    tok.insert(tok.end(), p.begin(), p.end());
+    off.push_back((int64_t)tok.size());
+    out.push_back(o);
+  }
+};
+
+std::vector<int32_t> id_run(int64_t base, int64_t n) {
+  if (base < 0 || base + n > kIdMax) throw std::runtime_error("workload: token id space exhausted");
+  std::vector<int32_t> v((size_t)n);
+  for (int64_t i = 0; i < n; ++i) v[(size_t)i] = (int32_t)(base + i);
+  return v;
+}
+
+int64_t span(int64_t lo, int64_t hi, std::mt19937_64& rng) {
+  return lo == hi ? lo : std::uniform_int_distribution<int64_t>(lo, hi)(rng);
+}
+
+void check(const e2_workload_spec& s) {
+  if (s.request_count < 0) throw std::invalid_argument("workload: request_count must be >= 0");
+  if (s.system_prompt_len < 0 || s.branch_len < 0 || s.observation_len < 0)
+    throw std::invalid_argument("workload: lengths must be >= 0");
+  if (s.unique_min < 0 || s.unique_min > s.unique_max)
+    throw std::invalid_argument("workload: unique_suffix_len range is invalid");
+  if (s.output_min < 1 || s.output_min > s.output_max)
+    throw std::invalid_argument("workload: output_len range must satisfy 1 <= min <= max");
+  switch (s.archetype) {
+    case E2_ARCH_CUSTOM:
+    case E2_ARCH_TOOLBENCH:
+      if (s.branch_count < 1) throw std::invalid_argument("workload: branch_count must be >= 1");
+      if (s.zipf && s.zipf_s <= 0) throw std::invalid_argument("workload: zipf_s must be > 0");
+      if (s.system_prompt_len + s.branch_len + s.unique_min < 1)
+        throw std::invalid_argument("workload: prompts would be empty");
+      break;
+    case E2_ARCH_PROGRAMMING:
+    case E2_ARCH_VIDEO_QA:
+    case E2_ARCH_DOC_QA:
+    case E2_ARCH_TREE_OF_THOUGHT:
+      if (s.requests_per_group < 1.0) throw std::invalid_argument("workload: requests_per_group must be >= 1");
+      if (s.branch_len < 1) throw std::invalid_argument("workload: grouped trunks need branch_len >= 1");
+      break;
+    case E2_ARCH_EMBODIED:
+      if (s.chain_mean_len < 2.0) throw std::invalid_argument("workload: chain_mean_len must be >= 2");
+      if (s.branch_len < 1) throw std::invalid_argument("workload: chain roots need branch_len >= 1");
+      break;
+    default:
+      throw std::invalid_argument("workload: unknown archetype");
+  }
+}
+
+void build(const e2_workload_spec& s, uint64_t seed, Builder& b) {
+  check(s);
+  std::mt19937_64 rng(seed);
+  const std::vector<int32_t> sys = id_run(kSys, s.system_prompt_len);
+  const int64_t N = s.request_count;
+  switch (s.archetype) {
+    case E2_ARCH_CUSTOM:
+    case E2_ARCH_TOOLBENCH: {
+      const int nb = (int)s.branch_count;
+      std::vector<double> cdf;
+      if (s.zipf) {
+        double acc = 0;
+        for (int k = 1; k <= nb; ++k) {
+          acc += std::pow((double)k, -s.zipf_s);
+          cdf.push_back(acc);
+        }
+        for (double& c : cdf) c /= acc;
+      }
+      std::uniform_int_distribution<int> pick(0, nb - 1);
+      for (int64_t i = 0; i < N; ++i) {
+        int br;
+        if (s.zipf) {
+          const double u = std::uniform_real_distribution<double>(0.0, 1.0)(rng);
+          br = (int)std::min<std::ptrdiff_t>(std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin(), nb - 1);
+        } else {
+          br = pick(rng);
+        }
+        std::vector<int32_t> p = sys;
+        const std::vector<int32_t> trunk = id_run(kTrunk + (int64_t)br * s.branch_len, s.branch_len);
+        p.insert(p.end(), trunk.begin(), trunk.end());
+        b.fresh_ids(p, span(s.unique_min, s.unique_max, rng));
+        b.emit(p, span(s.output_min, s.output_max, rng));
+      }
+      break;
+    }
+    case E2_ARCH_PROGRAMMING:
+    case E2_ARCH_VIDEO_QA:
+    case E2_ARCH_DOC_QA: {
+      std::poisson_distribution<int64_t> extra(std::max(0.0, s.requests_per_group - 1.0));
+      int64_t made = 0, trunk_base = kTrunk, group = 0;
+      const bool varlen = s.branch_len_max > s.branch_len;
+      while (made < N) {
+        int64_t size = s.archetype == E2_ARCH_PROGRAMMING ? std::llround(s.requests_per_group) : 1 + extra(rng);
+        size = std::min(size, N - made);
+        const int64_t tl = varlen ? span(s.branch_len, s.branch_len_max, rng) : s.branch_len;
+        const int64_t base = varlen ? trunk_base : kTrunk + group * s.branch_len;
+        const std::vector<int32_t> trunk = id_run(base, tl);
+        for (int64_t j = 0; j < size; ++j) {
+          std::vector<int32_t> p = sys;
+          p.insert(p.end(), trunk.begin(), trunk.end());
+          b.fresh_ids(p, span(s.unique_min, s.unique_max, rng));
+          b.emit(p, span(s.output_min, s.output_max, rng));
+        }
+        made += size;
+        trunk_base += tl;
+        ++group;
+      }
+      break;
+    }
+    case E2_ARCH_EMBODIED: {
+      std::geometric_distribution<int64_t> extra(1.0 / (s.chain_mean_len - 2.0 + 1.0));
+      int64_t made = 0;
+      while (made < N) {
+        int64_t steps = std::min<int64_t>(2 + extra(rng), N - made);
+        std::vector<int32_t> ctx;
+        b.fresh_ids(ctx, s.branch_len);
+        for (int64_t k = 0; k < steps; ++k) {
+          const int64_t o = span(s.output_min, s.output_max, rng);
+          b.emit(ctx, o);
+          if (k + 1 < steps) {
+            b.fresh_ids(ctx, o);
+            b.fresh_ids(ctx, s.observation_len);
+          }
+        }
+        made += steps;
+      }
+      break;
+    }
+    case E2_ARCH_TREE_OF_THOUGHT: {
+      // Problems arrive in blocks of requests_per_group; each request follows
+      // a random root-to-node path of a fanout^depth thought tree whose
+      // segments get fresh token ids on first visit.
+      const int64_t per = std::max<int64_t>(1, std::llround(s.requests_per_group));
+      const int64_t fan = std::max<int64_t>(1, s.fanout), dep = std::max<int64_t>(1, s.depth);
+      int64_t made = 0, group = 0;
+      while (made < N) {
+        const int64_t size = std::min(per, N - made);
+        const std::vector<int32_t> trunk = id_run(kTrunk + group * s.branch_len, s.branch_len);
+        std::map<std::vector<int64_t>, std::vector<int32_t>> seg;
+        for (int64_t j = 0; j < size; ++j) {
+          std::vector<int32_t> p = sys;
+          p.insert(p.end(), trunk.begin(), trunk.end());
+          const int64_t k = span(1, dep, rng);
+          std::vector<int64_t> path;
+          for (int64_t l = 0; l < k; ++l) {
+            path.push_back(span(0, fan - 1, rng));
+            auto it = seg.find(path);
+            if (it == seg.end()) {
+              std::vector<int32_t> v;
+              b.fresh_ids(v, span(s.unique_min, s.unique_max, rng));
+              it = seg.emplace(path, std::move(v)).first;
+            }
+            p.insert(p.end(), it->second.begin(), it->second.end());
+          }
+          b.emit(p, span(s.output_min, s.output_max, rng));
+        }
+        made += size;
+        ++group;
+      }
+      break;
+    }
+  }
+}
+
+}  // namespace
+
+void e2_set_global_error(const char* m);
+
+extern "C" {
+
+void e2_workload_default(int32_t archetype, e2_workload_spec* o) {
+  memset(o, 0, sizeof(*o));
+  o->archetype = archetype;
+  o->request_count = 1000;
+  o->branch_count = 1;
+  o->zipf_s = 1.1;
+  o->output_min = o->output_max = 32;
+  // archetype_default (workload.cpp:133-194)
+  switch (archetype) {
+    case E2_ARCH_TOOLBENCH:
+      o->system_prompt_len = 200;
+      o->branch_count = 16;
+      o->branch_len = 1660;
+      o->zipf = 1;
+      o->unique_min = 120;
+      o->unique_max = 220;
+      o->output_min = 40;
+      o->output_max = 56;
+      break;
+    case E2_ARCH_EMBODIED:
+      o->branch_len = 500;
+      o->chain_mean_len = 5.0;
+      o->observation_len = 300;
+      o->output_min = 6;
+      o->output_max = 14;
+      break;
+    case E2_ARCH_PROGRAMMING:
+      o->system_prompt_len = 2000;
+      o->branch_len = 2000;
+      o->requests_per_group = 8.0;
+      o->unique_min = 150;
+      o->unique_max = 250;
+      o->output_min = 180;
+      o->output_max = 240;
+      break;
+    case E2_ARCH_VIDEO_QA:
+      o->branch_len = 14500;
+      o->requests_per_group = 8.5;
+      o->unique_min = 400;
+      o->unique_max = 600;
+      o->output_min = o->output_max = 6;
+      break;
+    case E2_ARCH_DOC_QA:
+      o->system_prompt_len = 13;
+      o->branch_len = 6000;
+      o->requests_per_group = 6.0;
+      o->unique_min = 200;
+      o->unique_max = 300;
+      o->output_min = 20;
+      o->output_max = 30;
+      break;
+    case E2_ARCH_TREE_OF_THOUGHT:
+      o->system_prompt_len = 1000;
+      o->branch_len = 500;
+      o->requests_per_group = 64.0;
+      o->fanout = 3;
+      o->depth = 8;
+      o->unique_min = 40;
+      o->unique_max = 120;
+      o->output_min = 40;
+      o->output_max = 120;
+      break;
+    default:
+      break;
+  }
+  o->branch_len_max = o->branch_len;
+}
+
+int e2_generate(const e2_workload_spec* spec, uint64_t seed, double rps, uint64_t arrival_seed, int64_t* n_requests,
+                int64_t* n_tokens, int32_t* tokens, int64_t* offsets, int64_t* ids, double* arrivals,
+                int64_t* output_lens) {
+  try {
+    if (!(rps > 0)) throw std::invalid_argument("workload: requests_per_second must be > 0");
+    Builder b;
+    build(*spec, seed, b);
+    const int64_t n = (int64_t)b.out.size();
+    *n_requests = n;
+    *n_tokens = (int64_t)b.tok.size();
+    if (!tokens) return E2_OK;
+    std::copy(b.tok.begin(), b.tok.end(), tokens);
+    std::copy(b.off.begin(), b.off.end(), offsets);
+    std::mt19937_64 rng(arrival_seed);
+    std::exponential_distribution<double> gap(rps / 1000.0);
+    double t = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      t += gap(rng);
+      arrivals[i] = t;
+      ids[i] = i + 1;
+      output_lens[i] = b.out[(size_t)i];
+    }
+    return E2_OK;
+  } catch (const std::exception& e) {
+    e2_set_global_error(e.what());
+    return E2_ERR_CONFIG;
+  }
+}
+
+}  // extern "C"
