@@ -132,6 +132,11 @@ typedef struct e2_handle e2_handle;
 int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* model,
               const e2_policy* policy, e2_handle** out);
 void e2_destroy(e2_handle* h);
+/* Return h to its just-created state, keeping its allocations (bench steps). */
+int e2_reset(e2_handle* h);
+/* Product only: enqueue all device work of h on `stream` (a cudaStream_t);
+ * NULL restores the handle's own stream. */
+int e2_set_stream(e2_handle* h, void* stream);
 /* Message of the last failed call on h (or of the last failed e2_create
  * when h is NULL). */
 const char* e2_last_error(const e2_handle* h);

@@ -29,6 +29,7 @@ using namespace kvsched;
 
 struct e2_handle {
   std::unique_ptr<GlobalScheduler> s;
+  GlobalPolicy policy;
   int n = 0;
   std::string err;
 };
@@ -162,6 +163,7 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     h->s = std::make_unique<GlobalScheduler>(n_gpus, to_cfg(cfg), to_model(model),
                                              to_policy(policy));
     h->n = n_gpus;
+    h->policy = to_policy(policy);
     *out = h.release();
     return E2_OK;
   } catch (const ConfigError& e) {
@@ -174,6 +176,19 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
 }
 
 void e2_destroy(e2_handle* h) { delete h; }
+
+int e2_reset(e2_handle* h) {
+  return guard(h, [&] {
+    SchedulerConfig c = h->s->config();
+    TimeModel m = h->s->model();
+    GlobalPolicy p;
+    // GlobalScheduler has no policy() accessor: keep the one it was built with
+    p = h->policy;
+    h->s = std::make_unique<GlobalScheduler>(h->n, c, m, p);
+  });
+}
+
+int e2_set_stream(e2_handle*, void*) { return E2_OK; }
 
 const char* e2_last_error(const e2_handle* h) {
   return h ? h->err.c_str() : g_create_err.c_str();

@@ -169,6 +169,8 @@ _i32, _i64, _u64, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes
 _SIGS = {
     "e2_create": (ctypes.c_int, [_i32, P(SchedCfg), P(TimeModelC), P(PolicyC), P(_h)]),
     "e2_destroy": (None, [_h]),
+    "e2_reset": (ctypes.c_int, [_h]),
+    "e2_set_stream": (ctypes.c_int, [_h, _vp]),
     "e2_last_error": (ctypes.c_char_p, [_h]),
     "e2_backend": (ctypes.c_char_p, []),
     "e2_schedule": (ctypes.c_int, [_h, _vp, _i64, _i64, _f64, _f64, P(DecisionC), _vp, _vp]),

@@ -265,6 +265,7 @@ struct e2_handle {
   e2_time_model model;
   e2_policy pol;
   Stream stream = 0;
+  Stream own_stream_handle = 0;
   bool own_stream = false;
   // token arena
   i32* tok = nullptr;
@@ -286,6 +287,13 @@ struct e2_handle {
   unsigned long long* d_bytes = nullptr;  // [0] match bytes, [1] group bytes
   ApiOut* d_api = nullptr;
   ApiOut api;
+  // resident staging for host-buffer replays
+  i64 st_cap = 0, st_cost_cap = 0, st_rat_cap = 0;
+  i64 *st_ids = nullptr, *st_out = nullptr, *st_offs = nullptr;
+  double* st_arr = nullptr;
+  e2_decision* st_dec = nullptr;
+  e2_cost* st_cost = nullptr;
+  double* st_rat = nullptr;
   // autoscale queue stats (global_scheduler.hpp:157-158): host-side, fed by
   // note_admitted; prefix root id -> bucket -> (sum, count)
   std::map<u64, std::map<i64, std::pair<double, i64>>> queue_stats;
@@ -317,7 +325,6 @@ struct Timed {
   int k;
   cudaEvent_t a = nullptr, b = nullptr;
   Timed(e2_handle* hh, int kk) : h(hh), k(kk) {
-    h->acc.launches[k]++;
     if (h->prof) {
       a = ev_get(h);
       b = ev_get(h);
@@ -345,7 +352,7 @@ void prof_flush(e2_handle* h) {
 }
 #else
 struct Timed {
-  Timed(e2_handle* h, int k) { h->acc.launches[k]++; }
+  Timed(e2_handle*, int) {}
 };
 void prof_flush(e2_handle*) {}
 #endif
@@ -669,6 +676,7 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
   {
     Timed t(h, a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER);
 #if E2_DEVICE_BUILD
+    h->acc.launches[a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER]++;
     k_serial<<<1, 32, 0, h->stream>>>(h->d, a);
     CK(cudaGetLastError());
 #else
@@ -689,6 +697,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   {
     Timed t(h, E2_K_MATCH);
     unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
+    h->acc.launches[E2_K_MATCH]++;
     k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(d, n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
                                                              h->b_dm, h->d_bytes);
     CK(cudaGetLastError());
@@ -704,11 +713,13 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   const unsigned tg = (unsigned)((n + 255) / 256);
   dset(h->g_tk, 0, tsz * 8, h->stream);
   dset(h->g_tv, 0xff, tsz * 4, h->stream);
+  h->acc.launches[E2_K_GROUP]++;
   k_group_init<<<tg, 256, 0, h->stream>>>(d, n, base, h->r_off, h->r_len, h->b_S, h->b_dslot, h->b_dm, h->b_state,
                                           h->b_A, h->b_B, h->b_cand, h->b_L, h->g_tk, h->g_tv, h->g_mask);
   CK(cudaGetLastError());
   for (int round = 0;; ++round) {
     dset(h->d_cnt, 0, 8, h->stream);
+    h->acc.launches[E2_K_GROUP]++;
     k_group_resolve<<<tg, 256, 0, h->stream>>>(n, round, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
                                                h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_cnt, h->d_cnt + 1);
     CK(cudaGetLastError());
@@ -720,6 +731,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
     dset(h->g_tk, 0, tsz * 8, h->stream);
     dset(h->g_tv, 0xff, tsz * 4, h->stream);
     unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
+    h->acc.launches[E2_K_GROUP]++;
     k_group_round<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(
         d, n, base, round + 1, h->r_off, h->r_len, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
         h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_bytes + 1);
@@ -1120,6 +1132,7 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     h->d.cfg = c;
 #if E2_DEVICE_BUILD
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream_handle = h->stream;
     h->own_stream = true;
 #endif
     h->d.hot_g = talloc<Hot>(1);
@@ -1157,7 +1170,8 @@ void e2_destroy(e2_handle* h) {
                   d.free_pages, d.inf_key, d.inf_gpu, d.inf_cached, d.inf_prompt, d.inf_arr, d.inf_root, d.fifo_req,
                   d.fifo_tail, d.scr_slot, d.scr_val, d.scr_la, d.scr_id, d.vic_slot, d.vic_tok, d.hot_g, h->tok,
                   h->r_off, h->r_len, h->b_S, h->b_L, h->b_cand, h->b_leader, h->b_o, h->b_dslot, h->b_dm,
-                  h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api};
+                  h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api,
+                  h->st_ids, h->st_out, h->st_offs, h->st_arr, h->st_dec, h->st_cost, h->st_rat};
   for (void* p : ptrs) dfree(p);
 #if E2_DEVICE_BUILD
   for (auto& e : h->ev) {
@@ -1165,12 +1179,54 @@ void e2_destroy(e2_handle* h) {
     cudaEventDestroy(e.second.second);
   }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
-  if (h->own_stream) cudaStreamDestroy(h->stream);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream_handle);
 #endif
   delete h;
 }
 
 const char* e2_last_error(const e2_handle* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int e2_reset(e2_handle* h) {
+  return guard(h, [&] {
+    Dev& d = h->d;
+    const int G = h->G;
+    const u64 used = h->hot.slots_used;
+    dset(d.hdr, 0, used * sizeof(NodeHdr), h->stream);
+    dset(d.cmask, 0, used * 8, h->stream);
+    dset(d.lamask, 0, used * 8, h->stream);
+    dset(d.nchild, 0, used * 4, h->stream);
+    dset(d.la, 0, used * G * 8, h->stream);
+    dset(d.hits, 0, used * G * 4, h->stream);
+    dset(d.ccc, 0, used * G * 4, h->stream);
+    dset(d.ck, 0xff, (d.ct_mask + 1) * 8, h->stream);
+    dset(d.pg_n, 0, (size_t)h->hot.pages_used * 4, h->stream);
+    std::vector<i64> empty(d.inf_mask + 1, kNoInflight);
+    h2d(d.inf_key, empty.data(), empty.size() * 8, h->stream);
+    memset(&h->hot, 0, sizeof(h->hot));
+    for (int g = 0; g < kMaxG; ++g) h->hot.redirect[g] = -1;
+    h->hot.next_id = 1;
+    h->hot.slots_used = 1;
+    NodeHdr root;
+    memset(&root, 0, sizeof(root));
+    root.parent = kNil;
+    h2d(d.hdr, &root, sizeof(root), h->stream);
+    push_hot(h);
+    ssync(h->stream);
+    h->tok_len = 0;
+    h->queue_stats.clear();
+  });
+}
+
+int e2_set_stream(e2_handle* h, void* stream) {
+  return guard(h, [&] {
+#if E2_DEVICE_BUILD
+    ssync(h->stream);
+    h->stream = stream ? (Stream)stream : h->own_stream_handle;
+#else
+    (void)stream;
+#endif
+  });
+}
 
 int e2_schedule(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t request_id, double arrival_ms,
                 double now, e2_decision* out, e2_cost* costs, double* ratios) {
@@ -1504,7 +1560,6 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     e2_decision* d_dec = nullptr;
     e2_cost* d_cost = nullptr;
     double* d_rat = nullptr;
-    std::vector<void*> owned;
     if (device_ptrs) {
       d_ids = (i64*)ids;
       d_arr = (double*)arrivals;
@@ -1514,20 +1569,32 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
       d_cost = costs;
       d_rat = ratios;
     } else {
-      d_ids = talloc<i64>(n);
-      d_arr = talloc<double>(n);
-      d_out = talloc<i64>(n);
-      d_offs = talloc<i64>(n + 1);
-      d_dec = talloc<e2_decision>(n);
-      owned = {d_ids, d_arr, d_out, d_offs, d_dec};
-      if (costs) {
-        d_cost = talloc<e2_cost>((size_t)n * (G + 1));
-        owned.push_back(d_cost);
+      if (n > h->st_cap) {
+        for (void* p : {(void*)h->st_ids, (void*)h->st_out, (void*)h->st_offs, (void*)h->st_arr, (void*)h->st_dec}) dfree(p);
+        h->st_ids = talloc<i64>(n);
+        h->st_arr = talloc<double>(n);
+        h->st_out = talloc<i64>(n);
+        h->st_offs = talloc<i64>(n + 1);
+        h->st_dec = talloc<e2_decision>(n);
+        h->st_cap = n;
       }
-      if (ratios) {
-        d_rat = talloc<double>((size_t)n * G);
-        owned.push_back(d_rat);
+      if (costs && n * (G + 1) > h->st_cost_cap) {
+        dfree(h->st_cost);
+        h->st_cost = talloc<e2_cost>((size_t)n * (G + 1));
+        h->st_cost_cap = n * (G + 1);
       }
+      if (ratios && n * G > h->st_rat_cap) {
+        dfree(h->st_rat);
+        h->st_rat = talloc<double>((size_t)n * G);
+        h->st_rat_cap = n * G;
+      }
+      d_ids = h->st_ids;
+      d_arr = h->st_arr;
+      d_out = h->st_out;
+      d_offs = h->st_offs;
+      d_dec = h->st_dec;
+      d_cost = costs ? h->st_cost : nullptr;
+      d_rat = ratios ? h->st_rat : nullptr;
       h2d(d_ids, ids, n * 8, h->stream);
       h2d(d_arr, arrivals, n * 8, h->stream);
       h2d(d_out, output_lens, n * 8, h->stream);
@@ -1536,6 +1603,7 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
 #if E2_DEVICE_BUILD
     {
       Timed t(h, E2_K_OTHER);
+      h->acc.launches[E2_K_OTHER]++;
       k_arena_index<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(n, tstart, d_offs, h->r_off, h->r_len, 0);
       CK(cudaGetLastError());
     }
@@ -1595,7 +1663,6 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
       if (costs) d2h(costs, d_cost, (size_t)done * (G + 1) * sizeof(e2_cost), h->stream);
       if (ratios) d2h(ratios, d_rat, (size_t)done * G * 8, h->stream);
       ssync(h->stream);
-      for (void* p : owned) dfree(p);
     }
     if (n_done) *n_done = done;
     if (fail_code) throw Fail(fail_code, fail + " (request index " + std::to_string(done) + ")");

@@ -34,7 +34,7 @@ E2_D i64 warp_lcp(const i32* a, const i32* b, i64 lim) {
       i64 i = base + l + 32 * k;
       in[k] = i < lim;
       av[k] = in[k] ? __ldg(a + i) : 0;
-      bv[k] = in[k] ? __ldg(b + i) : 0;
+      bv[k] = in[k] ? __ldcs(b + i) : 0;  // prompt side streams (evict-first in L2)
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
