@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 from . import abi
-from .scheduler import DriverConfig, SchedulerConfig
+from .scheduler import DriverConfig, GlobalPolicy, SchedulerConfig
 
 ARCH = {
     "custom": 0,
@@ -92,6 +92,7 @@ class Config:
     rps: float = 2000.0
     arrival_seed: int = 14
     spec_overrides: dict = dataclasses.field(default_factory=dict)
+    policy: Optional[GlobalPolicy] = None
 
     def spec(self, lib=None) -> abi.WorkloadSpecC:
         s = default_spec(self.archetype, lib)
@@ -123,10 +124,11 @@ CONFIGS = {
         "c2_toolbench_100k_8inst", "toolbench", 100000, 8, _cs2_sched(),
         DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=1860, high_water=150000, finish_lag=2000),
     ),
-    # C3: LooGLE-shape doc QA: docs U[20000,40000], questions U[200,300], 1+Poisson(5) per doc, 16 instances.
+    # C3: LooGLE-shape doc QA: docs U[20000,40000], questions U[200,300], 1+Poisson(5) per doc,
+    # 16 instances; cap 100k / high-water 0.9 so the eviction term M is active.
     "c3": Config(
-        "c3_docqa_20k-40k_16inst", "doc_qa", 10000, 16, _cs2_sched(cap=200000),
-        DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=150000, finish_lag=2000),
+        "c3_docqa_20k-40k_16inst", "doc_qa", 10000, 16, _cs2_sched(cap=100000),
+        DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=90000, finish_lag=2000),
         spec_overrides=dict(branch_len=20000, branch_len_max=40000),
     ),
 }

@@ -1,0 +1,92 @@
+"""Replay parity: the product engine vs the unmodified reference on the same
+synthetic traces — every decision field, every cost term bit-for-bit, and
+the final mirror (ids, parents, edges, caching, last_access, windowed hits).
+
+CPU runs use the host emulation build of the engine; the `gpu` variants run
+the identical cases (and the full-size configs) through libe2sched.so.
+"""
+from __future__ import annotations
+
+import copy
+import dataclasses
+
+import pytest
+
+from paper_2407_00023_b200 import abi, workload as W
+from paper_2407_00023_b200.scheduler import DriverConfig, GlobalPolicy, SchedulerConfig
+
+from parity import assert_same_state, diff_decisions, replay
+
+
+def _cfg(name, arch, n, G, cap, hw, evict, H=10000.0, batch=0, trunk=0, policy=None, **over):
+    c = W.Config(
+        name,
+        arch,
+        n,
+        G,
+        SchedulerConfig(kv_capacity_tokens=cap, history_window_ms=H),
+        DriverConfig(eviction=evict, trunk_len=trunk, high_water=hw, finish_lag=min(2000, n // 4), batch=batch),
+        spec_overrides=over,
+    )
+    c.policy = policy
+    return c
+
+
+LRU, FIFO = abi.E2_EVICT_MIRROR_LRU, abi.E2_EVICT_FIFO_TAIL
+
+CASES = {
+    "c1": W.CONFIGS["c1"],
+    "c1_batch7": dataclasses.replace(W.CONFIGS["c1"], driver=dataclasses.replace(W.CONFIGS["c1"].driver, batch=7)),
+    "c2_5k": dataclasses.replace(W.CONFIGS["c2"], n_requests=5000),
+    "toolbench_lru_tight": _cfg("tb_tight", "toolbench", 3000, 4, 30000, 22000, LRU, batch=256),
+    "docqa_mterm": _cfg("docqa", "doc_qa", 1500, 16, 60000, 57000, LRU, batch=128),
+    "docqa_varlen": _cfg("docqa_var", "doc_qa", 600, 8, 90000, 70000, LRU, branch_len=3000, branch_len_max=9000),
+    "programming_mterm": _cfg("prog", "programming", 2000, 8, 20000, 19000, LRU, batch=512),
+    "programming_infeasible": _cfg("prog_inf", "programming", 800, 4, 6000, 5700, LRU, batch=100),
+    "embodied_chains": _cfg("emb", "embodied_agent", 1500, 4, 30000, 28500, LRU, batch=64),
+    "videoqa_fifo": _cfg("vqa", "video_qa", 600, 4, 80000, 60000, FIFO, trunk=14500),
+    "tot_deep": _cfg("tot", "tree_of_thought", 1500, 8, 20000, 19000, LRU, batch=200),
+    "round_robin": _cfg("rr", "toolbench", 800, 3, 200000, 150000, FIFO, trunk=1860,
+                        policy=GlobalPolicy(mode=1)),
+    "no_rebalance_no_pd": _cfg("nrb", "programming", 1200, 4, 30000, 20000, LRU,
+                               policy=GlobalPolicy(rebalance=False, pd_balance=False)),
+    "short_window": _cfg("shortH", "doc_qa", 1200, 8, 60000, 57000, LRU, H=300.0),
+}
+
+
+def _run_case(lib, ref_lib, gen_lib, case):
+    cfg = CASES[case]
+    trace = cfg.trace(lib=gen_lib)
+    sa, a = replay(ref_lib, cfg, trace)
+    sb, b = replay(lib, cfg, trace)
+    assert getattr(a, "error", None) is None, a.error
+    d = diff_decisions(a, b)
+    assert d is None, f"first mismatch at request {d[0]} field {d[1]}"
+    assert a.n_done == trace.n
+    assert_same_state(sa, sb, float(trace.arrivals[-1]))
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_replay_parity_hostsim(hostsim_lib, ref_lib, gen_lib, case):
+    _run_case(hostsim_lib, ref_lib, gen_lib, case)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_replay_parity_b200(b200_lib, ref_lib, gen_lib, case):
+    _run_case(b200_lib, ref_lib, gen_lib, case)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n", [("c1", None), ("c2", None), ("c3", 3000)])
+def test_full_config_parity_b200(b200_lib, ref_lib, gen_lib, name, n):
+    """BASELINE.json configs at full size (C3 on a prefix: the reference's
+    plan_eviction dominates its runtime)."""
+    cfg = W.CONFIGS[name]
+    trace = cfg.trace(lib=gen_lib, n_requests=n)
+    sa, a = replay(ref_lib, cfg, trace, want_ratios=False)
+    sb, b = replay(b200_lib, cfg, trace, want_ratios=False)
+    d = diff_decisions(a, b)
+    assert d is None, f"first mismatch at request {d[0]} field {d[1]}"
+    assert a.n_done == b.n_done == trace.n
+    assert_same_state(sa, sb, float(trace.arrivals[-1]))
