@@ -46,7 +46,10 @@ void* dalloc(size_t n) {
   void* p = nullptr;
   if (n == 0) n = 8;
   CK(cudaMalloc(&p, n));
+  // the handle's stream is non-blocking: finish the zero-fill before any
+  // async upload on that stream can land in this buffer
   CK(cudaMemset(p, 0, n));
+  CK(cudaDeviceSynchronize());
   return p;
 }
 void dfree(void* p) {
