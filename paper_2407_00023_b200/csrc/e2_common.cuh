@@ -91,6 +91,22 @@ inline double i2d(i64 v) { return (double)v; }
 
 E2_HD bool lane0() { return lane() == 0; }
 
+// Warp vote over positions [0, n) (n <= 32): bit j = f(j).  On the device
+// lane j evaluates f(j); the host emulation loops, so both builds probe the
+// same 32-wide windows.
+template <typename F>
+E2_D u32 vote(int n, F&& f) {
+#if E2_DEVICE_BUILD
+  const int l = lane();
+  return ballot(l < n && f(l));
+#else
+  u32 m = 0;
+  for (int j = 0; j < n; ++j)
+    if (f(j)) m |= 1u << j;
+  return m;
+#endif
+}
+
 template <typename T>
 E2_HDX T min_(T a, T b) { return a < b ? a : b; }
 template <typename T>

@@ -4,9 +4,9 @@
 // Every operation reproduces one reference call with identical state
 // effects; floating point uses explicit round-to-nearest intrinsics in the
 // reference's operation order.  Token comparisons never happen here: every
-// walk is given its matched length by the batched match kernels (K1 + the
-// intra-batch leader rounds, e2_match.cuh), so a walk costs one child-table
-// probe per tree level.
+// walk is given its matched length (and K1's path hints) by the batched
+// match kernels (e2_match.cuh), so a walk costs no child-table probe when
+// the hinted path is still current.
 #pragma once
 
 #include "e2_tree.cuh"
@@ -27,11 +27,10 @@ struct Scr {
 
 // Result of a node-level walk with a known matched length.
 struct Walk {
-  u32 last;       // deepest node touched (kRoot when nothing matched)
-  i64 last_m;     // tokens matched inside `last`
-  i64 cached_len; // Σ spans cached somewhere (prefix_tree.cpp:104-106)
-  u64 present;    // gpus with a per_gpu_matched_len entry (first span's set)
-  u32 first;      // first-level node (kNil when nothing matched)
+  u32 last;        // deepest node touched (kRoot when nothing matched)
+  i64 last_m;      // tokens matched inside `last`
+  i64 cached_len;  // Σ spans cached somewhere (prefix_tree.cpp:104-106)
+  u64 present;     // gpus with a per_gpu_matched_len entry (first span's set)
   bool ok;
 };
 
@@ -40,35 +39,38 @@ struct Walk {
 // ---------------------------------------------------------------------------
 E2_HD u64 wslot(const Dev& d, int g, u64 i) { return (u64)g * d.wcap + (i & (d.wcap - 1)); }
 
-// hits(n, g) counts in-window requests placed on g whose prompt passes
-// through n: undo a request's stamps when it leaves g's window.
-E2_HD void hits_dec_chain(const Dev& d, u32 tail, int g) {
-  const int G = d.cfg.G;
-  for (u32 n = tail; n != kRoot && n != kNil; n = d.hdr[n].parent) d.hits[(u64)n * G + g] -= 1;
-}
+constexpr double kInf = __builtin_huge_val();
 
 // prune (cost_model.cpp:31-42): inclusive horizon, t >= now - H survives.
+// Hit stamps of pruned entries are undone lazily (hits_catchup).
 E2_HD void win_prune(const Dev& d, Hot* h, int g, double now) {
   const double cutoff = dsub(now, d.cfg.H);
-  u64 hd = h->ws_head[g], tl = h->ws_tail[g];
-  while (hd < tl) {
-    u64 i = wslot(d, g, hd);
-    if (!(d.ws_t[i] < cutoff)) break;
-    const i64 m = d.ws_missed[i];
-    h->ws_missed_sum[g] -= m;
-    if (m > 0) h->ws_missed_nz[g] -= 1;
-    hits_dec_chain(d, d.ws_slot[i], g);
-    hd++;
+  if (h->ws_head_t[g] < cutoff) {
+    u64 hd = h->ws_head[g];
+    const u64 tl = h->ws_tail[g];
+    double t = h->ws_head_t[g];
+    while (hd < tl && t < cutoff) {
+      const i64 m = d.win[wslot(d, g, hd)].missed;
+      h->ws_missed_sum[g] -= m;
+      if (m > 0) h->ws_missed_nz[g] -= 1;
+      hd++;
+      t = hd < tl ? d.win[wslot(d, g, hd)].t : kInf;
+    }
+    h->ws_head[g] = hd;
+    h->ws_head_t[g] = t;
   }
-  h->ws_head[g] = hd;
-  u64 ch = h->wc_head[g], ct = h->wc_tail[g];
-  while (ch < ct) {
-    u64 i = wslot(d, g, ch);
-    if (!(d.wc_t[i] < cutoff)) break;
-    h->wc_output_sum[g] -= d.wc_out[i];
-    ch++;
+  if (h->wc_head_t[g] < cutoff) {
+    u64 ch = h->wc_head[g];
+    const u64 ct = h->wc_tail[g];
+    double t = h->wc_head_t[g];
+    while (ch < ct && t < cutoff) {
+      h->wc_output_sum[g] -= d.comp[wslot(d, g, ch)].out;
+      ch++;
+      t = ch < ct ? d.comp[wslot(d, g, ch)].t : kInf;
+    }
+    h->wc_head[g] = ch;
+    h->wc_head_t[g] = t;
   }
-  h->wc_head[g] = ch;
 }
 
 // load_ms (cost_model.cpp:65-73) — prefill folded from integer sums, decode
@@ -78,23 +80,26 @@ E2_HD double win_load(const Dev& d, Hot* h, int g, double now) {
   const Cfg& c = d.cfg;
   const i64 nsched = (i64)(h->ws_tail[g] - h->ws_head[g]);
   const i64 ncomp = (i64)(h->wc_tail[g] - h->wc_head[g]);
-  double prefill = dadd(dmul(c.c0, i2d(h->ws_missed_nz[g])), dmul(c.c1, i2d(h->ws_missed_sum[g])));
-  double avg = ncomp == 0 ? i2d(c.default_out) : ddiv(i2d(h->wc_output_sum[g]), i2d(ncomp));
-  double decode = dmul(i2d(nsched), dmul(c.c2, avg));
+  const double prefill = dadd(dmul(c.c0, i2d(h->ws_missed_nz[g])), dmul(c.c1, i2d(h->ws_missed_sum[g])));
+  const double avg = ncomp == 0 ? i2d(c.default_out) : ddiv(i2d(h->wc_output_sum[g]), i2d(ncomp));
+  const double decode = dmul(i2d(nsched), dmul(c.c2, avg));
   return dadd(prefill, decode);
 }
 
 E2_HD bool win_add_sched(const Dev& d, Hot* h, int g, double now, i64 missed, i64 est, u32 tail) {
-  u64 t = h->ws_tail[g];
-  if (t - h->ws_head[g] >= d.wcap) {
+  const u64 t = h->ws_tail[g];
+  if (t - h->ws_done[g] >= d.wcap) {
     set_err(h, kErrCapacity, kWhyWindowCap);
     return false;
   }
-  u64 i = wslot(d, g, t);
-  d.ws_t[i] = now;
-  d.ws_missed[i] = missed;
-  d.ws_est[i] = est;
-  d.ws_slot[i] = tail;
+  WinEnt e;
+  e.t = now;
+  e.missed = missed;
+  e.est = est;
+  e.slot = tail;
+  e.pad = 0;
+  d.win[wslot(d, g, t)] = e;
+  if (t == h->ws_head[g]) h->ws_head_t[g] = now;
   h->ws_tail[g] = t + 1;
   h->ws_missed_sum[g] += missed;
   if (missed > 0) h->ws_missed_nz[g] += 1;
@@ -102,17 +107,45 @@ E2_HD bool win_add_sched(const Dev& d, Hot* h, int g, double now, i64 missed, i6
 }
 
 E2_HD bool win_add_comp(const Dev& d, Hot* h, int g, double now, i64 out) {
-  u64 t = h->wc_tail[g];
+  const u64 t = h->wc_tail[g];
   if (t - h->wc_head[g] >= d.wcap) {
     set_err(h, kErrCapacity, kWhyWindowCap);
     return false;
   }
-  u64 i = wslot(d, g, t);
-  d.wc_t[i] = now;
-  d.wc_out[i] = out;
+  CompEnt e;
+  e.t = now;
+  e.out = out;
+  d.comp[wslot(d, g, t)] = e;
+  if (t == h->wc_head[g]) h->wc_head_t[g] = now;
   h->wc_tail[g] = t + 1;
   h->wc_output_sum[g] += out;
   return true;
+}
+
+// hits(n, g) counts in-window requests placed on g whose prompt passes
+// through n.  Undo the stamps of requests that left g's
+// window since the last catch-up, walking each one's path from its tail
+// slot (splits since then put the copied stamps on the new prefix nodes,
+// which the parent walk visits too).  Warp-wide.
+E2_D void hits_catchup(Ctx& x, int g) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
+  const int G = d.cfg.G;
+  while (h->ws_done[g] < h->ws_head[g]) {
+    const u32 tail = d.win[wslot(d, g, h->ws_done[g])].slot;
+    for (u32 n = tail; n != kRoot && n != kNil;) {
+      NodeRec* r = nget(x, n);
+      const u32 p = r->parent;
+      if (lane0()) {
+        rhits(r, G)[g] -= 1;
+        ndirty(x, r);
+      }
+      wsync();
+      n = p;
+    }
+    if (lane0()) h->ws_done[g]++;
+    wsync();
+  }
 }
 
 E2_HD double prefill_time(const Cfg& c, i64 missed) {
@@ -122,14 +155,16 @@ E2_HD double prefill_time(const Cfg& c, i64 missed) {
 
 // ---------------------------------------------------------------------------
 // Eviction planning — PrefixTree::plan_eviction (prefix_tree.cpp:273-308).
-// Single-lane, read-only on the tree; per-instance scratch holds the
+// Single-lane, read-only on the tree (npeek); per-instance scratch holds the
 // surfaced-parent work list (sorted) and the simulated cached-child counts.
 // visit(slot, tokens) is called per plan entry in plan order.
 // Returns freed tokens.
 // ---------------------------------------------------------------------------
 template <typename Visit>
-E2_HD i64 plan_eviction(const Dev& d, Hot* h, int g, i64 need, bool partial, Visit&& visit) {
+E2_HD i64 plan_eviction(const Ctx& x, int g, i64 need, bool partial, Visit&& visit) {
   if (need <= 0) return 0;
+  const Dev& d = x.d;
+  Hot* h = x.h;
   const int G = d.cfg.G;
   const u32 half = d.scap / 2;
   u32* s_slot = d.scr_slot + (u64)g * d.scap;  // [0,half): surfaced list, [half,scap): sim ccc
@@ -141,18 +176,19 @@ E2_HD i64 plan_eviction(const Dev& d, Hot* h, int g, i64 need, bool partial, Vis
   u32 k = 0, j = 0, page = kNil;
   i32 pcnt = 0;
   if (nd > 0) {
-    page = d.dir_page[dring(d, h, g, 0)];
-    pcnt = d.pg_n[page];
+    const DirEntry e = d.dir[dring(d, h, g, 0)];
+    page = e.page;
+    pcnt = e.cnt;
   }
   i64 freed = 0;
   while (freed < need) {
-    bool have_a = page != kNil;
-    bool have_b = nsurf_head < ns;
+    const bool have_a = page != kNil;
+    const bool have_b = nsurf_head < ns;
     if (!have_a && !have_b) break;
     u32 v;
     bool take_b = false;
     if (have_a && have_b) {
-      u64 ai = (u64)page * kPage + j;
+      const u64 ai = (u64)page * kPage + j;
       take_b = kless(s_la[nsurf_head], s_id[nsurf_head], d.pg_la[ai], d.pg_id[ai]);
     } else {
       take_b = have_b;
@@ -164,46 +200,50 @@ E2_HD i64 plan_eviction(const Dev& d, Hot* h, int g, i64 need, bool partial, Vis
       if (++j >= (u32)pcnt) {
         j = 0;
         if (++k < nd) {
-          page = d.dir_page[dring(d, h, g, k)];
-          pcnt = d.pg_n[page];
+          const DirEntry e = d.dir[dring(d, h, g, k)];
+          page = e.page;
+          pcnt = e.cnt;
         } else {
           page = kNil;
         }
       }
     }
-    const i64 tok = d.hdr[v].edge_len;
+    const NodeRec* rv = npeek(x, v);
+    const i64 tok = rv->edge_len;
     const i64 remaining = need - freed;
     if (partial && tok > remaining) {
-      visit(v, remaining);
+      visit(v, remaining, rv);
       freed += remaining;
       break;
     }
-    visit(v, tok);
+    visit(v, tok, rv);
     freed += tok;
-    const u32 p = d.hdr[v].parent;
-    if (p != kNil && p != kRoot && cached_on(d, p, g)) {
-      u32 x = 0;
-      while (x < nsim && s_slot[half + x] != p) ++x;
+    const u32 p = rv->parent;
+    if (p != kNil && p != kRoot) {
+      const NodeRec* rp = npeek(x, p);
+      if (!rcached(rp, g)) continue;
+      u32 xi = 0;
+      while (xi < nsim && s_slot[half + xi] != p) ++xi;
       i64 c;
-      if (x < nsim) {
-        c = s_val[half + x] - 1;
+      if (xi < nsim) {
+        c = s_val[half + xi] - 1;
       } else {
         if (nsim >= d.scap - half) {
           set_err(h, kErrCapacity, kWhyScratchCap);
           break;
         }
-        c = (i64)d.ccc[(u64)p * G + g] - 1;
+        c = (i64)rccc(rp, G)[g] - 1;
         s_slot[half + nsim] = p;
         nsim++;
       }
-      s_val[half + x] = c;
+      s_val[half + xi] = c;
       if (c == 0) {
         // sorted insert into the pending part of the surfaced list
         if (ns >= half) {
           set_err(h, kErrCapacity, kWhyScratchCap);
           break;
         }
-        const u64 pla = la_bits(d, p, g), pid = d.hdr[p].id;
+        const u64 pla = dbits(rla(rp)[g]), pid = rp->id;
         u32 pos = ns;
         while (pos > nsurf_head && kless(pla, pid, s_la[pos - 1], s_id[pos - 1])) {
           s_la[pos] = s_la[pos - 1];
@@ -221,13 +261,16 @@ E2_HD i64 plan_eviction(const Dev& d, Hot* h, int g, i64 need, bool partial, Vis
   return freed;
 }
 
-// load_cost (cost_model.cpp:75-100).  Single-lane.
+// load_cost (cost_model.cpp:75-100).  Single-lane; when need > 0 the
+// caller has run hits_catchup(g) (cost_prepare).
 struct CostOut {
   double L, M, P;
   bool inf;
 };
 
-E2_HD CostOut cost_for(const Dev& d, Hot* h, int g, i64 missed, double now) {
+E2_HD CostOut cost_for(const Ctx& x, int g, i64 missed, double now) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   CostOut o;
   o.L = win_load(d, h, g, now);
   o.P = prefill_time(d.cfg, missed);
@@ -240,9 +283,9 @@ E2_HD CostOut cost_for(const Dev& d, Hot* h, int g, i64 missed, double now) {
     const Cfg& c = d.cfg;
     const int G = c.G;
     double M = 0.0;
-    i64 freed = plan_eviction(d, h, g, need, false, [&](u32 v, i64 tok) {
+    const i64 freed = plan_eviction(x, g, need, false, [&](u32, i64 tok, const NodeRec* rv) {
       if (total > 0) {
-        const double nj = ddiv(i2d(d.hits[(u64)v * G + g]), i2d(total));
+        const double nj = ddiv(i2d(rhits(rv, G)[g]), i2d(total));
         M = dadd(M, dmul(prefill_time(c, tok), nj));
       }
     });
@@ -252,17 +295,26 @@ E2_HD CostOut cost_for(const Dev& d, Hot* h, int g, i64 missed, double now) {
   return o;
 }
 
+// Warp-wide: make g's windowed hit counters current before a cost with an
+// eviction term is evaluated.
+E2_D void cost_prepare(Ctx& x, int g, i64 missed, double now) {
+  if (lane0()) win_prune(x.d, x.h, g, now);
+  wsync();
+  if (missed - (x.d.cfg.cap - x.h->cached_tokens[g]) > 0) hits_catchup(x, g);
+}
+
 // ---------------------------------------------------------------------------
 // Walks (warp-wide).  `L` = matched length of the sequence against the
-// current tree, from the batched match; prefix_tree.cpp:79-114.
+// current tree, from the batched match; prefix_tree.cpp:79-114.  `hint`
+// holds K1's path slots (may be stale after in-batch splits; validated).
 // ---------------------------------------------------------------------------
-E2_D Walk walk_known(const Dev& d, const i32* seq, i64 L, i64* ext) {
+E2_D Walk walk_known(Ctx& x, const i32* seq, i64 L, const u32* hint, int nhint, i64* ext) {
+  const Dev& d = x.d;
   Walk w;
   w.last = kRoot;
   w.last_m = 0;
   w.cached_len = 0;
   w.present = 0;
-  w.first = kNil;
   w.ok = true;
   const int G = d.cfg.G;
   for (int g = lane(); g < G; g += kWidth) ext[g] = 0;
@@ -270,19 +322,29 @@ E2_D Walk walk_known(const Dev& d, const i32* seq, i64 L, i64* ext) {
   bool first_span = true;
   i64 pos = 0;
   u32 cur = kRoot;
+  int level = 0;
   while (pos < L) {
-    u32 ch = child_lookup(d, cur, seq[pos]);
+    const i32 t = seq[pos];
+    u32 ch = kNil;
+    if (level < nhint) {
+      const u32 c = hint[level];
+      if (c != kNil) {
+        const NodeRec* rc = nget(x, c);
+        if (rc->parent == cur && rc->first_tok == t && rc->edge_len > 0) ch = c;
+      }
+    }
+    if (ch == kNil) ch = child_lookup(d, cur, t);
     if (ch == kNil) {
       w.ok = false;
       break;
     }
-    const i64 len = d.hdr[ch].edge_len;
+    const NodeRec* r = nget(x, ch);
+    const i64 len = r->edge_len;
     const i64 m = min_(len, L - pos);
-    const u64 cm = d.cmask[ch];
+    const u64 cm = r->cmask;
     if (first_span) {
       alive = cm;
       w.present = cm;
-      w.first = ch;
       first_span = false;
     } else {
       alive &= cm;
@@ -294,6 +356,7 @@ E2_D Walk walk_known(const Dev& d, const i32* seq, i64 L, i64* ext) {
     cur = ch;
     w.last = ch;
     w.last_m = m;
+    level++;
     if (m < len) break;
   }
   wsync();
@@ -302,27 +365,29 @@ E2_D Walk walk_known(const Dev& d, const i32* seq, i64 L, i64* ext) {
 
 // ensure_path (prefix_tree.cpp:156-185) given the walk of the same sequence.
 // Returns the node whose edge ends exactly at |seq| (kNil on error).
-E2_D u32 ensure_path(const Dev& d, Hot* h, i64 seq_off, i64 n, i64 L, const Walk& w) {
+E2_D u32 ensure_path(Ctx& x, i64 seq_off, i64 n, i64 L, const Walk& w) {
   u32 cur = (L == 0) ? kRoot : w.last;
-  if (L > 0 && w.last_m < (i64)d.hdr[w.last].edge_len) {
-    cur = split_node(d, h, w.last, (u32)w.last_m);
+  if (L > 0 && w.last_m < (i64)nget(x, w.last)->edge_len) {
+    cur = split_node(x, w.last, (u32)w.last_m);
     if (cur == kNil) return kNil;
   }
   if (L == n) return cur;
-  return new_leaf(d, h, cur, seq_off + L, (u32)(n - L), (u32)L);
+  return new_leaf(x, cur, seq_off + L, (u32)(n - L), (u32)L);
 }
 
 // ---------------------------------------------------------------------------
 // Redirect upkeep — update_redirects (global_scheduler.cpp:194-219).  Warp-wide.
 // ---------------------------------------------------------------------------
-E2_D void update_redirects(const Dev& d, Hot* h, Scr* s, double now) {
+E2_D void update_redirects(Ctx& x, Scr* s, double now) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   const int G = d.cfg.G;
   for (int g = lane(); g < G; g += kWidth) s->loads[g] = win_load(d, h, g, now);
   wsync();
   if (lane0()) {
     const double th = d.cfg.th_bal;
     for (int src = 0; src < G; ++src) {
-      int dst = h->redirect[src];
+      const int dst = h->redirect[src];
       if (dst >= 0 && s->loads[src] <= dmul(th, s->loads[dst])) h->redirect[src] = -1;
     }
     int hi = 0, lo = 0;
@@ -346,7 +411,7 @@ E2_HD int pick_min(const Scr* s, int n) {
   double bt = 0;
   for (int i = 0; i < n; ++i) {
     if (s->cinf[i]) continue;
-    double t = dadd(dadd(s->cL[i], s->cM[i]), s->cP[i]);
+    const double t = dadd(dadd(s->cL[i], s->cM[i]), s->cP[i]);
     if (best < 0 || t < bt) {
       best = s->cgpu[i];
       bt = t;
@@ -354,7 +419,7 @@ E2_HD int pick_min(const Scr* s, int n) {
   }
   if (best >= 0) return best;
   for (int i = 0; i < n; ++i) {
-    double t = dadd(dadd(s->cL[i], s->cM[i]), s->cP[i]);
+    const double t = dadd(dadd(s->cL[i], s->cM[i]), s->cP[i]);
     if (best < 0 || t < bt) {
       best = s->cgpu[i];
       bt = t;
@@ -370,9 +435,19 @@ struct Dec {
   i32 ok;  // 0 = error raised
 };
 
+E2_HD void put_cost(Scr* s, int idx, int g, const CostOut& c) {
+  s->cgpu[idx] = g;
+  s->cL[idx] = c.L;
+  s->cM[idx] = c.M;
+  s->cP[idx] = c.P;
+  s->cinf[idx] = c.inf ? 1 : 0;
+}
+
 // decide (global_scheduler.cpp:76-158).  Warp-wide.  Fills s->c* and
 // s->ratios; w receives the walk for a following commit.
-E2_D Dec decide(const Dev& d, Hot* h, Scr* s, const i32* seq, i64 n, i64 L, double now, Walk& w) {
+E2_D Dec decide(Ctx& x, Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, double now, Walk& w) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   Dec r;
   r.branch = 1;
   r.gpu = -1;
@@ -403,7 +478,7 @@ E2_D Dec decide(const Dev& d, Hot* h, Scr* s, const i32* seq, i64 n, i64 L, doub
   }
   if (lane0()) h->stats[kStTreeReads]++;
   wsync();
-  w = walk_known(d, seq, L, s->ext);
+  w = walk_known(x, seq, L, hint, nhint, s->ext);
   if (!w.ok) {
     if (lane0()) set_err(h, kErrSim, kWhyWalk);
     wsync();
@@ -419,21 +494,20 @@ E2_D Dec decide(const Dev& d, Hot* h, Scr* s, const i32* seq, i64 n, i64 L, doub
   if (r.missed_len < r.cached_len) {
     r.branch = 0;
     i64 best = 0;
-    for (int g = 0; g < G; ++g)
-      if (((w.present >> g) & 1ull) && s->ext[g] > best) best = s->ext[g];
-    // candidates in ascending gpu order; lanes evaluate their own instances
+    for (u64 m = w.present; m; m &= m - 1) best = max_(best, s->ext[ffs64(m)]);
     u64 cand = 0;
-    for (int g = 0; g < G; ++g)
-      if (((w.present >> g) & 1ull) && s->ext[g] == best) cand |= (1ull << g);
+    for (u64 m = w.present; m; m &= m - 1) {
+      const int g = ffs64(m);
+      if (s->ext[g] == best) cand |= (1ull << g);
+    }
+    for (u64 m = cand; m; m &= m - 1) {
+      const int g = ffs64(m);
+      cost_prepare(x, g, n - s->ext[g], now);
+    }
     for (int g = lane(); g < G; g += kWidth) {
       if ((cand >> g) & 1ull) {
-        int idx = popc64(cand & ((1ull << g) - 1));
-        CostOut c = cost_for(d, h, g, n - s->ext[g], now);
-        s->cgpu[idx] = g;
-        s->cL[idx] = c.L;
-        s->cM[idx] = c.M;
-        s->cP[idx] = c.P;
-        s->cinf[idx] = c.inf ? 1 : 0;
+        const int idx = popc64(cand & ((1ull << g) - 1));
+        put_cost(s, idx, g, cost_for(x, g, n - s->ext[g], now));
       }
     }
     wsync();
@@ -445,14 +519,8 @@ E2_D Dec decide(const Dev& d, Hot* h, Scr* s, const i32* seq, i64 n, i64 L, doub
       for (int i = 0; i < nc; ++i)
         if (s->cgpu[i] == t) ti = i;
       if (ti < 0) {
-        if (lane0()) {
-          CostOut c = cost_for(d, h, t, n - s->ext[t], now);
-          s->cgpu[nc] = t;
-          s->cL[nc] = c.L;
-          s->cM[nc] = c.M;
-          s->cP[nc] = c.P;
-          s->cinf[nc] = c.inf ? 1 : 0;
-        }
+        cost_prepare(x, t, n - s->ext[t], now);
+        if (lane0()) put_cost(s, nc, t, cost_for(x, t, n - s->ext[t], now));
         wsync();
         ti = nc;
         nc++;
@@ -486,14 +554,8 @@ E2_D Dec decide(const Dev& d, Hot* h, Scr* s, const i32* seq, i64 n, i64 L, doub
       r.gpu = max_g;
     } else {
       r.branch = 1;
-      for (int g = lane(); g < G; g += kWidth) {
-        CostOut c = cost_for(d, h, g, n - s->ext[g], now);
-        s->cgpu[g] = g;
-        s->cL[g] = c.L;
-        s->cM[g] = c.M;
-        s->cP[g] = c.P;
-        s->cinf[g] = c.inf ? 1 : 0;
-      }
+      for (int g = 0; g < G; ++g) cost_prepare(x, g, n - s->ext[g], now);
+      for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(x, g, n - s->ext[g], now));
       wsync();
       if (lane0()) s->n_costs = G;
       wsync();
@@ -516,18 +578,18 @@ E2_D Dec decide(const Dev& d, Hot* h, Scr* s, const i32* seq, i64 n, i64 L, doub
 
 // ---------------------------------------------------------------------------
 // Inflight map: request id -> placement (global_scheduler.hpp:129-135).
-// Single-lane; linear probing with backward-shift deletion.
+// Single-lane; linear probing with backward-shift deletion; 64-byte records.
 // ---------------------------------------------------------------------------
 E2_HD u64 inf_find(const Dev& d, i64 id, bool& found) {
   u64 i = mix64((u64)id) & d.inf_mask;
   for (u64 k = 0; k <= d.inf_mask; ++k, i = (i + 1) & d.inf_mask) {
-    i64 key = d.inf_key[i];
-    if (key == id && key != kNoInflight) {
-      found = true;
-      return i;
-    }
+    const i64 key = d.inf[i].key;
     if (key == kNoInflight) {
       found = false;
+      return i;
+    }
+    if (key == id) {
+      found = true;
       return i;
     }
   }
@@ -539,27 +601,24 @@ E2_HD void inf_erase_at(const Dev& d, u64 i) {
   u64 j = i;
   for (;;) {
     j = (j + 1) & d.inf_mask;
-    i64 key = d.inf_key[j];
-    if (key == kNoInflight) break;
-    u64 home = mix64((u64)key) & d.inf_mask;
+    const InfRec rj = d.inf[j];
+    if (rj.key == kNoInflight) break;
+    const u64 home = mix64((u64)rj.key) & d.inf_mask;
     // move j into the hole at i if home is not cyclically in (i, j]
-    bool in_range = (i <= j) ? (home > i && home <= j) : (home > i || home <= j);
+    const bool in_range = (i <= j) ? (home > i && home <= j) : (home > i || home <= j);
     if (!in_range) {
-      d.inf_key[i] = key;
-      d.inf_gpu[i] = d.inf_gpu[j];
-      d.inf_cached[i] = d.inf_cached[j];
-      d.inf_prompt[i] = d.inf_prompt[j];
-      d.inf_arr[i] = d.inf_arr[j];
-      d.inf_root[i] = d.inf_root[j];
+      d.inf[i] = rj;
       i = j;
     }
   }
-  d.inf_key[i] = kNoInflight;
+  d.inf[i].key = kNoInflight;
 }
 
 // commit (global_scheduler.cpp:160-175).  Warp-wide.  Returns the tail slot.
-E2_D u32 commit(const Dev& d, Hot* h, i64 seq_off, const i32* seq, i64 n, i64 L, const Walk& w,
-                const Dec& r, i64 req_id, double arrival, double now) {
+E2_D u32 commit(Ctx& x, i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
+                double now) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   if (d.cfg.mode == 1) {
     if (lane0()) h->rr_next++;
     wsync();
@@ -570,27 +629,30 @@ E2_D u32 commit(const Dev& d, Hot* h, i64 seq_off, const i32* seq, i64 n, i64 L,
     wsync();
     return kNil;
   }
-  (void)seq;
-  u32 tail = ensure_path(d, h, seq_off, n, L, w);
+  const u32 tail = ensure_path(x, seq_off, n, L, w);
   if (tail == kNil || h->err) return kNil;
   const int g = r.gpu;
   const int G = d.cfg.G;
   // record_hit bottom-up (prefix_tree.cpp:193-196)
-  u32 first = tail;
-  for (u32 x = tail; x != kRoot; x = d.hdr[x].parent) {
-    first = x;
-    if (lane0()) d.hits[(u64)x * G + g] += 1;
+  u64 root_id = 0;
+  for (u32 v = tail; v != kRoot;) {
+    NodeRec* rv = nget(x, v);
+    const u32 p = rv->parent;
+    root_id = rv->id;
+    if (lane0()) {
+      rhits(rv, G)[g] += 1;
+      ndirty(x, rv);
+    }
     wsync();
-    touch_la(d, h, x, g, now);
+    touch_la(x, v, g, now);
+    v = p;
   }
-  const u64 root_id = d.hdr[first].id;
-  wsync();
   if (lane0()) {
     win_add_sched(d, h, g, now, r.moc, d.cfg.default_out, tail);
     h->inflight_cached[g] += r.cached_len;
     h->inflight_prompt[g] += n;
     bool found;
-    u64 i = inf_find(d, req_id, found);
+    const u64 i = inf_find(d, req_id, found);
     if (i == ~0ull) {
       set_err(h, kErrCapacity, kWhyInflightCap);
     } else {
@@ -598,12 +660,16 @@ E2_D u32 commit(const Dev& d, Hot* h, i64 seq_off, const i32* seq, i64 n, i64 L,
         h->inflight_n++;
         if ((u64)h->inflight_n * 2 > d.inf_mask + 1) set_err(h, kErrCapacity, kWhyInflightCap);
       }
-      d.inf_key[i] = req_id;
-      d.inf_gpu[i] = g;
-      d.inf_cached[i] = r.cached_len;
-      d.inf_prompt[i] = n;
-      d.inf_arr[i] = arrival;
-      d.inf_root[i] = root_id;
+      InfRec e;
+      e.key = req_id;
+      e.gpu = g;
+      e.pad = 0;
+      e.cached = r.cached_len;
+      e.prompt = n;
+      e.arr = arrival;
+      e.root = root_id;
+      e.pad2 = 0;
+      d.inf[i] = e;
     }
   }
   wsync();
@@ -620,23 +686,26 @@ E2_D void count_stats(Hot* h, const Dec& r) {
 }
 
 // mark_cached_path bottom-up part (prefix_tree.cpp:203-211) from a known tail.
-E2_D void mark_cached_chain(const Dev& d, Hot* h, u32 tail, int g, double now) {
-  for (u32 x = tail; x != kRoot; x = d.hdr[x].parent) {
-    set_cached(d, h, x, g);
-    touch_la(d, h, x, g, now);
+E2_D void mark_cached_chain(Ctx& x, u32 tail, int g, double now) {
+  for (u32 v = tail; v != kRoot;) {
+    set_cached(x, v, g);
+    touch_la(x, v, g, now);
+    v = nget(x, v)->parent;
   }
 }
 
 // note_finished (global_scheduler.cpp:361-369).  Warp-wide.
-E2_D void note_finished(const Dev& d, Hot* h, i64 id, double now, i64 out) {
+E2_D void note_finished(Ctx& x, i64 id, double now, i64 out) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   if (lane0()) {
     bool found;
-    u64 i = inf_find(d, id, found);
+    const u64 i = inf_find(d, id, found);
     if (found) {
-      const int g = d.inf_gpu[i];
-      win_add_comp(d, h, g, now, out);
-      h->inflight_cached[g] -= d.inf_cached[i];
-      h->inflight_prompt[g] -= d.inf_prompt[i];
+      const InfRec e = d.inf[i];
+      win_add_comp(d, h, e.gpu, now, out);
+      h->inflight_cached[e.gpu] -= e.cached;
+      h->inflight_prompt[e.gpu] -= e.prompt;
       inf_erase_at(d, i);
       h->inflight_n--;
     }
@@ -644,9 +713,30 @@ E2_D void note_finished(const Dev& d, Hot* h, i64 id, double now, i64 out) {
   wsync();
 }
 
+// Clear [start, end) of the root path ending at `bottom`, deepest first
+// (the second half of uncache_suffix, prefix_tree.cpp:262-270).  The node
+// containing `start` has already been split there.
+E2_D i64 clear_range_from(Ctx& x, u32 bottom, i64 start, int g) {
+  i64 freed = 0;
+  for (u32 v = bottom; v != kRoot && v != kNil;) {
+    const NodeRec* r = nget(x, v);
+    const i64 v_end = (i64)r->depth + r->edge_len;
+    if (v_end <= start) break;
+    const u32 p = r->parent;
+    if (rcached(r, g)) {
+      freed += r->edge_len;
+      clear_cached(x, v, g);
+    }
+    v = p;
+  }
+  return freed;
+}
+
 // uncache_suffix (prefix_tree.cpp:237-271) for a sequence whose matched
 // length M is known.  Warp-wide.  Returns tokens uncached.
-E2_D i64 uncache_suffix(const Dev& d, Hot* h, const i32* seq, i64 n, i64 M, i64 tail_len, int g) {
+E2_D i64 uncache_suffix(Ctx& x, const i32* seq, i64 n, i64 M, i64 tail_len, int g) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   if (n == 0 || tail_len <= 0) return 0;
   const i64 end = min_(n, M);
   i64 start = n - tail_len;
@@ -656,49 +746,62 @@ E2_D i64 uncache_suffix(const Dev& d, Hot* h, const i32* seq, i64 n, i64 M, i64 
   i64 off = 0;
   u32 cur = kRoot, bottom = kNil;
   while (off < end) {
-    u32 ch = child_lookup(d, cur, seq[off]);
+    const u32 ch = child_lookup(d, cur, seq[off]);
     if (ch == kNil) {
       if (lane0()) set_err(h, kErrSim, kWhyWalk);
       wsync();
       return 0;
     }
-    const i64 len = d.hdr[ch].edge_len;
+    const i64 len = nget(x, ch)->edge_len;
     const i64 m = min_(len, M - off);
     u32 node = ch;
     if (m < len) {
-      node = split_node(d, h, ch, (u32)m);  // keep the part on seq's path
+      node = split_node(x, ch, (u32)m);  // keep the part on seq's path
       if (node == kNil) return 0;
     }
     const i64 node_end = off + m;
     if (node_end > start && off < start) {
       // split at start: the slot keeps the suffix, which is the target
-      u32 pre = split_node(d, h, node, (u32)(start - off));
-      if (pre == kNil) return 0;
+      if (split_node(x, node, (u32)(start - off)) == kNil) return 0;
     }
     bottom = node;
     cur = node;
     off = node_end;
     if (m < len) break;
   }
-  // clear deepest-first: bottom up to the node starting at `start`
-  i64 freed = 0;
-  for (u32 x = bottom; x != kRoot && x != kNil; x = d.hdr[x].parent) {
-    const i64 x_end = (i64)d.hdr[x].depth + d.hdr[x].edge_len;
-    if (x_end <= start) break;
-    if (cached_on(d, x, g)) {
-      freed += d.hdr[x].edge_len;
-      clear_cached(d, h, x, g);
+  return clear_range_from(x, bottom, start, g);
+}
+
+// uncache_suffix for a prompt committed earlier in this replay: its tail
+// slot (the node ending at |p|) is stable under splits, so the path is the
+// parent chain and no token is read.  Warp-wide.
+E2_D i64 uncache_tail(Ctx& x, u32 tail, i64 n, i64 tail_len, int g) {
+  if (n == 0 || tail_len <= 0 || tail == kNil) return 0;
+  i64 start = n - tail_len;
+  if (start < 0) start = 0;
+  if (start >= n) return 0;
+  // find the node containing `start` on the chain and split there
+  for (u32 v = tail; v != kRoot;) {
+    const NodeRec* r = nget(x, v);
+    const i64 dep = r->depth;
+    const u32 p = r->parent;
+    if (dep <= start) {
+      if (dep < start && split_node(x, v, (u32)(start - dep)) == kNil) return 0;
+      break;
     }
+    v = p;
   }
-  return freed;
+  return clear_range_from(x, tail, start, g);
 }
 
 // Mirror-LRU eviction: plan_eviction(g, over, {}, partial)
 // then note_eviction for every entry, ranges built before any is applied.
-E2_D void evict_lru(const Dev& d, Hot* h, int g, i64 over) {
+E2_D void evict_lru(Ctx& x, int g, i64 over) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   if (lane0()) {
     u32 nv = 0;
-    plan_eviction(d, h, g, over, true, [&](u32 v, i64 tok) {
+    plan_eviction(x, g, over, true, [&](u32 v, i64 tok, const NodeRec*) {
       if (nv < d.vcap) {
         d.vic_slot[nv] = v;
         d.vic_tok[nv] = tok;
@@ -712,13 +815,13 @@ E2_D void evict_lru(const Dev& d, Hot* h, int g, i64 over) {
   wsync();
   const u32 nv = (u32)d.scr_val[(u64)d.cfg.G * d.scap];
   for (u32 i = 0; i < nv && !h->err; ++i) {
-    u32 v = d.vic_slot[i];
+    const u32 v = d.vic_slot[i];
     const i64 tok = d.vic_tok[i];
-    const i64 len = d.hdr[v].edge_len;
+    const i64 len = nget(x, v)->edge_len;
     if (tok < len) {
-      if (split_node(d, h, v, (u32)(len - tok)) == kNil) return;
+      if (split_node(x, v, (u32)(len - tok)) == kNil) return;
     }
-    clear_cached(d, h, v, g);
+    clear_cached(x, v, g);
   }
 }
 

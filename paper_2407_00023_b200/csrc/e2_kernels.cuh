@@ -58,7 +58,8 @@ struct SerialArgs {
   const i64* ids;
   const double* arr;
   const i64* outl;
-  const i64* L;  // batch-local
+  const i64* L;     // batch-local
+  const u32* hint;  // batch-local K1 path hints [n][kPathHint]
   e2_decision* dec;
   e2_cost* costs;
   double* ratios;
@@ -66,6 +67,15 @@ struct SerialArgs {
   OpDesc op;
   ApiOut* out;
 };
+
+// Bring every instance's window and hit counters current at `now`
+// (export / dump / dead-node removal read hits for all instances).  Warp-wide.
+E2_D void expire_all(Ctx& x, double now) {
+  const int G = x.d.cfg.G;
+  for (int g = lane(); g < G; g += kWidth) win_prune(x.d, x.h, g, now);
+  wsync();
+  for (int g = 0; g < G; ++g) hits_catchup(x, g);
+}
 
 E2_D void write_decision(const Dev& d, const Scr* s, const Dec& r, i64 req_id, e2_decision* dec,
                          e2_cost* costs, double* ratios) {
@@ -105,38 +115,46 @@ E2_D void write_decision(const Dev& d, const Scr* s, const Dec& r, i64 req_id, e
 // Dead-node removal (prefix_tree.cpp:357-378): a node goes when it is
 // uncached, childless and has no in-window hit on any instance; repeat until
 // a fixpoint (the reference removes bottom-up in one DFS).  Warp-wide.
-E2_D i64 prune_dead(const Dev& d, Hot* h) {
+E2_D i64 prune_dead(Ctx& x) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   const int G = d.cfg.G;
   i64 removed = 0;
   bool again = true;
   while (again) {
     again = false;
     const u32 used = h->slots_used;
-    for (u32 b = 1; b < used; b += kWidth) {
-      u32 s = b + (u32)lane();
-      bool dead = false;
-      if (s < used) {
-        const NodeHdr hd = d.hdr[s];
-        if (hd.edge_len > 0 && d.cmask[s] == 0 && d.nchild[s] == 0) {
-          dead = true;
-          for (int g = 0; g < G; ++g)
-            if (d.hits[(u64)s * G + g] != 0) dead = false;
-        }
-      }
-      u32 m = ballot(dead);
+    for (u32 b = 1; b < used; b += 32) {
+      u32 m = vote(32, [&](int j) {
+        const u32 sl = b + (u32)j;
+        if (sl >= used) return false;
+        const NodeRec* r = npeek(x, sl);
+        if (r->edge_len == 0 || r->cmask != 0 || r->nchild != 0) return false;
+        for (int g = 0; g < G; ++g)
+          if (rhits(r, G)[g] != 0) return false;
+        return true;
+      });
+      wsync();
       while (m) {
-        int j = ffs32(m);
+        const int j = ffs32(m);
         m &= m - 1;
-        u32 x = b + (u32)j;
-        NodeHdr hx = d.hdr[x];
-        child_erase(d, h, hx.parent, hx.first_tok);
+        const u32 v = b + (u32)j;
+        NodeRec* rv = nget(x, v);
+        const u32 par = rv->parent;
+        const i32 ft = rv->first_tok;
+        wsync();
         if (lane0()) {
-          d.nchild[hx.parent] -= 1;
-          NodeHdr z = hx;
-          z.edge_len = 0;
-          z.parent = kNil;
-          d.hdr[x] = z;
+          rv->edge_len = 0;
+          rv->parent = kNil;
+          ndirty(x, rv);
           h->node_count--;
+        }
+        wsync();
+        child_erase(d, h, par, ft);
+        NodeRec* rp = nget(x, par);
+        if (lane0()) {
+          rp->nchild -= 1;
+          ndirty(x, rp);
         }
         wsync();
         removed++;
@@ -149,58 +167,67 @@ E2_D i64 prune_dead(const Dev& d, Hot* h) {
 
 // Subtree walks for autoscale replication (global_scheduler.cpp:299-338):
 // children are found by scanning parents (rare path).
-E2_D void subtree_apply(const Dev& d, Hot* h, u32 root, int g, double now, bool mark) {
-  // iterative DFS using the victim scratch as a stack
+E2_D void subtree_apply(Ctx& x, u32 root, int g, double now, bool mark) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   u32 top = 0;
   if (lane0()) d.vic_slot[0] = root;
   wsync();
   top = 1;
   u32 order = 0;
-  // collect the subtree (preorder) into vic_slot, then apply
+  // collect the subtree (breadth-first) into vic_slot, then apply
   while (order < top) {
-    u32 x = d.vic_slot[order++];
+    const u32 p = d.vic_slot[order++];
     const u32 used = h->slots_used;
-    for (u32 b = 1; b < used; b += kWidth) {
-      u32 s = b + (u32)lane();
-      bool ch = s < used && d.hdr[s].edge_len > 0 && d.hdr[s].parent == x;
-      u32 m = ballot(ch);
-      int cnt = popc32(m);
-      if (ch) {
-        int idx = popc32(m & ((1u << lane()) - 1));
-        d.vic_slot[top + idx] = s;
+    for (u32 b = 1; b < used; b += 32) {
+      const u32 m = vote(32, [&](int j) {
+        const u32 sl = b + (u32)j;
+        if (sl >= used) return false;
+        const NodeRec* r = npeek(x, sl);
+        return r->edge_len > 0 && r->parent == p;
+      });
+      wsync();
+      if (lane0()) {
+        u32 mm = m, t = top;
+        while (mm) {
+          d.vic_slot[t++] = b + (u32)ffs32(mm);
+          mm &= mm - 1;
+        }
       }
       wsync();
-      top += cnt;
+      top += (u32)popc32(m);
     }
   }
   if (mark) {
     for (u32 i = 0; i < top; ++i) {
-      u32 x = d.vic_slot[i];
-      if (x == kRoot) continue;
-      set_cached(d, h, x, g);
-      touch_la(d, h, x, g, now);
+      const u32 v = d.vic_slot[i];
+      if (v == kRoot) continue;
+      set_cached(x, v, g);
+      touch_la(x, v, g, now);
     }
   } else {
     for (u32 i = top; i-- > 0;) {  // children before parents
-      u32 x = d.vic_slot[i];
-      if (x != kRoot) clear_cached(d, h, x, g);
+      const u32 v = d.vic_slot[i];
+      if (v != kRoot) clear_cached(x, v, g);
     }
   }
 }
 
-E2_D void api_op(const Dev& d, Hot* h, Scr* s, const OpDesc& op, ApiOut* out) {
+E2_D void api_op(Ctx& x, Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   const int G = d.cfg.G;
   const i32* seq = d.tok + op.off;
   switch (op.kind) {
     case OP_SCHEDULE:
     case OP_DECIDE: {
       const bool commit_it = op.kind == OP_SCHEDULE;
-      if (commit_it && d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(d, h, s, op.now);
+      if (commit_it && d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(x, s, op.now);
       Walk w;
-      Dec r = decide(d, h, s, seq, op.len, op.L, op.now, w);
+      Dec r = decide(x, s, seq, op.len, op.L, hint, kPathHint, op.now, w);
       if (!r.ok) return;
       if (commit_it) {
-        commit(d, h, op.off, seq, op.len, op.L, w, r, op.id, op.arr, op.now);
+        commit(x, op.off, op.len, op.L, w, r, op.id, op.arr, op.now);
         if (h->err) return;
         count_stats(h, r);
       }
@@ -209,30 +236,31 @@ E2_D void api_op(const Dev& d, Hot* h, Scr* s, const OpDesc& op, ApiOut* out) {
     }
     case OP_PREFILL: {
       if (d.cfg.mode != 0 || op.len == 0) break;
-      Walk w = walk_known(d, seq, op.L, s->ext);
+      Walk w = walk_known(x, seq, op.L, hint, kPathHint, s->ext);
       if (!w.ok) {
         if (lane0()) set_err(h, kErrSim, kWhyWalk);
         wsync();
         return;
       }
-      u32 tail = ensure_path(d, h, op.off, op.len, op.L, w);
+      u32 tail = ensure_path(x, op.off, op.len, op.L, w);
       if (tail == kNil || h->err) return;
-      mark_cached_chain(d, h, tail, op.gpu, op.now);
+      mark_cached_chain(x, tail, op.gpu, op.now);
       break;
     }
     case OP_EVICT: {
       if (d.cfg.mode != 0) break;
-      i64 f = uncache_suffix(d, h, seq, op.len, op.L, op.x, op.gpu);
+      i64 f = uncache_suffix(x, seq, op.len, op.L, op.x, op.gpu);
       if (lane0()) out->i0 = f;
       wsync();
       break;
     }
     case OP_FINISHED:
-      note_finished(d, h, op.id, op.now, op.x);
+      note_finished(x, op.id, op.now, op.x);
       break;
     case OP_LOAD_COST: {
+      cost_prepare(x, op.gpu, op.x, op.now);
       if (lane0()) {
-        CostOut c = cost_for(d, h, op.gpu, op.x, op.now);
+        CostOut c = cost_for(x, op.gpu, op.x, op.now);
         out->costs[0].gpu = op.gpu;
         out->costs[0].eviction_infeasible = c.inf ? 1 : 0;
         out->costs[0].current_load_ms = c.L;
@@ -248,7 +276,7 @@ E2_D void api_op(const Dev& d, Hot* h, Scr* s, const OpDesc& op, ApiOut* out) {
       break;
     }
     case OP_MATCH: {
-      Walk w = walk_known(d, seq, op.L, s->ext);
+      Walk w = walk_known(x, seq, op.L, hint, kPathHint, s->ext);
       for (int g = lane(); g < G; g += kWidth) out->ext[g] = ((w.present >> g) & 1ull) ? s->ext[g] : 0;
       if (lane0()) {
         out->i0 = op.L;
@@ -257,11 +285,9 @@ E2_D void api_op(const Dev& d, Hot* h, Scr* s, const OpDesc& op, ApiOut* out) {
       wsync();
       break;
     }
-    case OP_EXPIRE_ALL: {
-      for (int g = lane(); g < G; g += kWidth) win_prune(d, h, g, op.now);
-      wsync();
+    case OP_EXPIRE_ALL:
+      expire_all(x, op.now);
       break;
-    }
     case OP_WINDOW: {
       if (lane0()) {
         win_prune(d, h, op.gpu, op.now);
@@ -279,35 +305,34 @@ E2_D void api_op(const Dev& d, Hot* h, Scr* s, const OpDesc& op, ApiOut* out) {
         u64 i = inf_find(d, op.id, found);
         out->i0 = found ? 1 : 0;
         if (found) {
-          out->u0 = d.inf_root[i];
-          out->v = d.inf_arr[i];
-          out->i1 = d.inf_gpu[i];
+          out->u0 = d.inf[i].root;
+          out->v = d.inf[i].arr;
+          out->i1 = d.inf[i].gpu;
         }
       }
       wsync();
       break;
     }
     case OP_PRUNE_DEAD: {
-      for (int g = lane(); g < G; g += kWidth) win_prune(d, h, g, op.now);
-      wsync();
-      i64 rm = prune_dead(d, h);
+      expire_all(x, op.now);
+      i64 rm = prune_dead(x);
       if (lane0()) out->i0 = rm;
       wsync();
       break;
     }
     case OP_MARK_NODE: {
-      u32 x = (u32)op.x;
-      if (x != kRoot) {
-        set_cached(d, h, x, op.gpu);
-        touch_la(d, h, x, op.gpu, op.now);
+      u32 v = (u32)op.x;
+      if (v != kRoot) {
+        set_cached(x, v, op.gpu);
+        touch_la(x, v, op.gpu, op.now);
       }
       break;
     }
     case OP_MARK_SUBTREE:
-      subtree_apply(d, h, (u32)op.x, op.gpu, op.now, true);
+      subtree_apply(x, (u32)op.x, op.gpu, op.now, true);
       break;
     case OP_UNCACHE_SUBTREE:
-      subtree_apply(d, h, (u32)op.x, op.gpu, op.now, false);
+      subtree_apply(x, (u32)op.x, op.gpu, op.now, false);
       break;
     default:
       break;
@@ -315,7 +340,9 @@ E2_D void api_op(const Dev& d, Hot* h, Scr* s, const OpDesc& op, ApiOut* out) {
 }
 
 // One request of the generalised criterion-7 loop (e2sched.h, e2_replay).
-E2_D void replay_step(const Dev& d, Hot* h, Scr* s, const SerialArgs& a, i64 li) {
+E2_D void replay_step(Ctx& x, Scr* s, const SerialArgs& a, i64 li) {
+  const Dev& d = x.d;
+  Hot* h = x.h;
   const int G = d.cfg.G;
   const i64 r = a.base + li;
   const i64 off = a.off[r], n = a.len[r];
@@ -323,17 +350,18 @@ E2_D void replay_step(const Dev& d, Hot* h, Scr* s, const SerialArgs& a, i64 li)
   const double now = max_(h->drv_now, a.arr[r]);
   if (lane0()) h->drv_now = now;
   wsync();
-  if (d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(d, h, s, now);
+  if (d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(x, s, now);
   Walk w;
-  Dec dec = decide(d, h, s, seq, n, a.L[li], now, w);
+  Dec dec = decide(x, s, seq, n, a.L[li], a.hint + li * kPathHint, kPathHint, now, w);
   if (!dec.ok) return;
-  u32 tail = commit(d, h, off, seq, n, a.L[li], w, dec, a.ids[r], a.arr[r], now);
+  const u32 tail = commit(x, off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now);
   if (h->err) return;
+  if (lane0()) d.req_tail[r] = tail;
   count_stats(h, dec);
   write_decision(d, s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
                  a.ratios ? a.ratios + r * G : nullptr);
   const int g = dec.gpu;
-  if (a.prefill && d.cfg.mode == 0) mark_cached_chain(d, h, tail, g, now);
+  if (a.prefill && d.cfg.mode == 0) mark_cached_chain(x, tail, g, now);
   if (h->err) return;
   if (a.eviction == E2_EVICT_FIFO_TAIL) {
     if (lane0()) {
@@ -351,29 +379,27 @@ E2_D void replay_step(const Dev& d, Hot* h, Scr* s, const SerialArgs& a, i64 li)
       wsync();
       if (lane0()) h->fifo_head[g]++;
       wsync();
-      if (d.cfg.mode == 0) {
-        const i64 kn = a.len[k];
-        uncache_suffix(d, h, d.tok + a.off[k], kn, kn, tl, g);
-      }
+      if (d.cfg.mode == 0) uncache_tail(x, d.req_tail[k], a.len[k], tl, g);
     }
   } else if (a.eviction == E2_EVICT_MIRROR_LRU) {
     const i64 cached = h->cached_tokens[g];
-    if (cached > a.hw && d.cfg.mode == 0) evict_lru(d, h, g, cached - a.hw);
+    if (cached > a.hw && d.cfg.mode == 0) evict_lru(x, g, cached - a.hw);
   }
   if (h->err) return;
   if (li + a.base >= a.lag) {
     const i64 k = r - a.lag;
-    note_finished(d, h, a.ids[k], now, a.outl[k]);
+    note_finished(x, a.ids[k], now, a.outl[k]);
   }
 }
 
-E2_D void serial_body(const Dev& d, Hot* h, Scr* s, const SerialArgs& a) {
+E2_D void serial_body(Ctx& x, Scr* s, const SerialArgs& a) {
+  Hot* h = x.h;
   if (lane0()) h->done = 0;
   wsync();
   if (a.kind == 0) {
     i64 i = 0;
     for (; i < a.n; ++i) {
-      replay_step(d, h, s, a, i);
+      replay_step(x, s, a, i);
       if (h->err) {
         if (lane0()) h->err_req = a.base + i;
         wsync();
@@ -383,10 +409,11 @@ E2_D void serial_body(const Dev& d, Hot* h, Scr* s, const SerialArgs& a) {
     if (lane0()) h->done = i;
     wsync();
   } else {
-    api_op(d, h, s, a.op, a.out);
+    api_op(x, s, a.op, a.hint, a.out);
     if (lane0()) h->done = h->err ? 0 : 1;
     wsync();
   }
+  nflush(x);
 }
 
 }  // namespace e2

@@ -123,16 +123,36 @@ namespace {
 constexpr int kMatchWarpsPerBlock = 8;
 
 #if E2_DEVICE_BUILD
-__global__ void __launch_bounds__(32, 1) k_serial(Dev d, SerialArgs a) {
+__global__ void __launch_bounds__(32, 1) k_serial(Dev d, SerialArgs a, u32 nsets) {
   __shared__ Hot hs;
   __shared__ Scr ss;
+  __shared__ NCache nc;
+  extern __shared__ __align__(16) char dyn[];
+  const u32 ne = nsets * kWays;
   {
     const u64* src = (const u64*)d.hot_g;
     u64* dst = (u64*)&hs;
     for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
   }
+  if (threadIdx.x == 0) {
+    nc.nsets = nsets;
+    nc.clock = 0;
+    nc.tag = (u32*)dyn;
+    nc.tick = nc.tag + ne;
+    nc.dirty = nc.tick + ne;
+    nc.data = dyn + ((3 * ne * 4 + 15) / 16) * 16;
+  }
+  for (u32 i = threadIdx.x; i < ne; i += 32) {
+    ((u32*)dyn)[i] = kNil;
+    ((u32*)dyn)[ne + i] = 0;
+    ((u32*)dyn)[2 * ne + i] = 0;
+  }
   __syncwarp();
-  serial_body(d, &hs, &ss, a);
+  Ctx x;
+  x.d = d;
+  x.h = &hs;
+  x.c = &nc;
+  serial_body(x, &ss, a);
   __syncwarp();
   {
     const u64* src = (const u64*)&hs;
@@ -143,11 +163,11 @@ __global__ void __launch_bounds__(32, 1) k_serial(Dev d, SerialArgs a) {
 
 __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32) k_match(Dev d, i64 n, i64 base, const i64* off,
                                                                      const i64* len, i64* S, u32* dslot, u32* dm,
-                                                                     unsigned long long* bytes) {
+                                                                     u32* path, unsigned long long* bytes) {
   const i64 w = (i64)blockIdx.x * kMatchWarpsPerBlock + (threadIdx.x >> 5);
   if (w >= n) return;
   const i64 r = base + w;
-  MatchRes m = match_one(d, d.tok + off[r], len[r]);
+  MatchRes m = match_one(d, d.tok + off[r], len[r], path + w * kPathHint);
   if (lane0()) {
     S[w] = m.S;
     dslot[w] = m.div_slot;
@@ -280,7 +300,7 @@ struct e2_handle {
   // batch work arrays
   i64 bcap = 0;
   i64 *b_S = nullptr, *b_L = nullptr, *b_cand = nullptr, *b_leader = nullptr, *b_o = nullptr;
-  u32 *b_dslot = nullptr, *b_dm = nullptr;
+  u32 *b_dslot = nullptr, *b_dm = nullptr, *b_path = nullptr;
   i32* b_state = nullptr;
   u64 *b_A = nullptr, *b_B = nullptr;
   u64* g_tk = nullptr;
@@ -300,6 +320,9 @@ struct e2_handle {
   // autoscale queue stats (global_scheduler.hpp:157-158): host-side, fed by
   // note_admitted; prefix root id -> bucket -> (sum, count)
   std::map<u64, std::map<i64, std::pair<double, i64>>> queue_stats;
+  u32 nsets = 0;          // node-cache sets of the serial kernel
+  size_t serial_smem = 0;  // its dynamic shared memory
+  i64 req_cap = 0;         // d.req_tail capacity
   // profiling
   bool prof = false;
   e2_profile acc;
@@ -375,101 +398,73 @@ void zero_ptrs(Dev& d) {
 // ---- capacity management ---------------------------------------------------
 void host_rehash_ct(e2_handle* h, u64 new_cap) {
   Dev& d = h->d;
-  const u64 old_cap = d.ct_mask + 1;
-  std::vector<u64> ok(old_cap);
-  std::vector<u32> ov(old_cap);
-  if (d.ck) {
-    d2h(ok.data(), d.ck, old_cap * 8, h->stream);
-    d2h(ov.data(), d.cv, old_cap * 4, h->stream);
+  const u64 old_cap = d.ct ? d.ct_mask + 1 : 0;
+  std::vector<CtEntry> old(old_cap);
+  if (old_cap) {
+    d2h(old.data(), d.ct, old_cap * sizeof(CtEntry), h->stream);
     ssync(h->stream);
   }
-  std::vector<u64> nk(new_cap, kEmptyKey);
-  std::vector<u32> nv(new_cap, 0);
+  CtEntry empty;
+  empty.key = kEmptyKey;
+  empty.val = 0;
+  empty.pad = 0;
+  std::vector<CtEntry> nt(new_cap, empty);
   const u64 mask = new_cap - 1;
-  if (d.ck) {
-    for (u64 i = 0; i < old_cap; ++i) {
-      u64 k = ok[i];
-      if (k == kEmptyKey || k == kTombKey) continue;
-      u64 j = mix64(k) & mask;
-      while (nk[j] != kEmptyKey) j = (j + 1) & mask;
-      nk[j] = k;
-      nv[j] = ov[i];
-    }
+  for (u64 i = 0; i < old_cap; ++i) {
+    const u64 k = old[i].key;
+    if (k == kEmptyKey || k == kTombKey) continue;
+    u64 j = mix64(k) & mask;
+    while (nt[j].key != kEmptyKey) j = (j + 1) & mask;
+    nt[j] = old[i];
   }
-  dfree(d.ck);
-  dfree(d.cv);
-  d.ck = talloc<u64>(new_cap);
-  d.cv = talloc<u32>(new_cap);
-  h2d(d.ck, nk.data(), new_cap * 8, h->stream);
-  h2d(d.cv, nv.data(), new_cap * 4, h->stream);
+  dfree(d.ct);
+  d.ct = talloc<CtEntry>(new_cap);
+  h2d(d.ct, nt.data(), new_cap * sizeof(CtEntry), h->stream);
   ssync(h->stream);
   d.ct_mask = mask;
 }
 
 void reserve_nodes(e2_handle* h, u64 need) {
   Dev& d = h->d;
-  if (need <= d.node_cap && d.hdr) return;
+  if (need <= d.node_cap && d.rec) return;
   const int G = h->G;
   u64 cap = std::max<u64>(need, (u64)d.node_cap * 2);
   cap = std::max<u64>(cap, 1024);
   if (cap > 0xfffffff0ull) throw Fail(E2_ERR_ARG, "node capacity exceeds 32-bit slots");
   const u64 keep = h->hot.slots_used;
-  grow(d.hdr, keep, cap, h->stream);
-  grow(d.cmask, keep, cap, h->stream);
-  grow(d.lamask, keep, cap, h->stream);
-  grow(d.nchild, keep, cap, h->stream);
-  grow(d.la, keep * G, cap * G, h->stream);
-  grow(d.hits, keep * G, cap * G, h->stream);
-  grow(d.ccc, keep * G, cap * G, h->stream);
+  grow(d.rec, keep * d.rs, cap * d.rs, h->stream);
   d.node_cap = (u32)cap;
   // child table at load <= 1/2
-  u64 ct = pow2_at_least(2 * cap);
-  if (!d.ck || ct > d.ct_mask + 1) host_rehash_ct(h, ct);
+  const u64 ct = pow2_at_least(2 * cap);
+  if (!d.ct || ct > d.ct_mask + 1) host_rehash_ct(h, ct);
   // LRU pages: each page holds >= 1 key; keys <= cached nodes
-  u64 pages = cap / 2 + 1024 * (u64)G;
+  const u64 pages = cap / 2 + 1024 * (u64)G;
   if (pages > d.page_cap || !d.pg_la) {
     const u64 kp = h->hot.pages_used;
     grow(d.pg_la, kp * kPage, pages * kPage, h->stream);
     grow(d.pg_id, kp * kPage, pages * kPage, h->stream);
     grow(d.pg_slot, kp * kPage, pages * kPage, h->stream);
-    grow(d.pg_n, kp, pages, h->stream);
     grow(d.free_pages, h->hot.free_top, pages, h->stream);
     d.page_cap = (u32)pages;
   }
   // directory ring per instance
-  u64 dcap = pow2_at_least(std::max<u64>(cap / 8 + 1024, 1024));
+  const u64 dcap = pow2_at_least(std::max<u64>(cap / 8 + 1024, 1024));
   if (dcap > d.dcap) {
-    u32* np = talloc<u32>(dcap * G);
-    u64* nla = talloc<u64>(dcap * G);
-    u64* nid = talloc<u64>(dcap * G);
-    if (d.dir_page) {
-      std::vector<u32> op(d.dcap * (u64)G), pp(dcap * G, 0);
-      std::vector<u64> ol(d.dcap * (u64)G), oi(d.dcap * (u64)G), pl(dcap * G, 0), pi(dcap * G, 0);
-      d2h(op.data(), d.dir_page, op.size() * 4, h->stream);
-      d2h(ol.data(), d.dir_la, ol.size() * 8, h->stream);
-      d2h(oi.data(), d.dir_id, oi.size() * 8, h->stream);
+    DirEntry* nd = talloc<DirEntry>(dcap * G);
+    if (d.dir) {
+      std::vector<DirEntry> od(d.dcap * (u64)G), pd(dcap * G);
+      d2h(od.data(), d.dir, od.size() * sizeof(DirEntry), h->stream);
       ssync(h->stream);
       for (int g = 0; g < G; ++g) {
-        for (u32 k = 0; k < h->hot.dir_n[g]; ++k) {
-          u64 src = (u64)g * d.dcap + ((h->hot.dir_head[g] + k) & (d.dcap - 1));
-          u64 dst = (u64)g * dcap + k;
-          pp[dst] = op[src];
-          pl[dst] = ol[src];
-          pi[dst] = oi[src];
-        }
+        for (u32 k = 0; k < h->hot.dir_n[g]; ++k)
+          pd[(u64)g * dcap + k] = od[(u64)g * d.dcap + ((h->hot.dir_head[g] + k) & (d.dcap - 1))];
         h->hot.dir_head[g] = 0;
       }
-      h2d(np, pp.data(), pp.size() * 4, h->stream);
-      h2d(nla, pl.data(), pl.size() * 8, h->stream);
-      h2d(nid, pi.data(), pi.size() * 8, h->stream);
+      h2d(nd, pd.data(), pd.size() * sizeof(DirEntry), h->stream);
       ssync(h->stream);
-      dfree(d.dir_page);
-      dfree(d.dir_la);
-      dfree(d.dir_id);
+      dfree(d.dir);
     }
-    d.dir_page = np;
-    d.dir_la = nla;
-    d.dir_id = nid;
+    d.dir = nd;
     d.dcap = (u32)dcap;
     push_hot(h);
   }
@@ -506,14 +501,11 @@ void ring_regrow(e2_handle* h, T*& arr, u64 oldcap, u64 newcap, const u64* heads
 
 void reserve_window(e2_handle* h, u64 entries) {
   Dev& d = h->d;
-  u64 cap = pow2_at_least(std::max<u64>(entries, 1024));
+  const u64 cap = pow2_at_least(std::max<u64>(entries, 1024));
   if (cap <= d.wcap) return;
-  ring_regrow(h, d.ws_t, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
-  ring_regrow(h, d.ws_missed, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
-  ring_regrow(h, d.ws_est, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
-  ring_regrow(h, d.ws_slot, d.wcap, cap, h->hot.ws_head, h->hot.ws_tail);
-  ring_regrow(h, d.wc_t, d.wcap, cap, h->hot.wc_head, h->hot.wc_tail);
-  ring_regrow(h, d.wc_out, d.wcap, cap, h->hot.wc_head, h->hot.wc_tail);
+  // scheduled entries stay until their hit stamps are undone (ws_done)
+  ring_regrow(h, d.win, d.wcap, cap, h->hot.ws_done, h->hot.ws_tail);
+  ring_regrow(h, d.comp, d.wcap, cap, h->hot.wc_head, h->hot.wc_tail);
   d.wcap = cap;
 }
 
@@ -528,56 +520,28 @@ void reserve_fifo(e2_handle* h, u64 entries) {
 
 void reserve_inflight(e2_handle* h, u64 live) {
   Dev& d = h->d;
-  u64 cap = pow2_at_least(std::max<u64>(4 * live + 64, 1024));
-  if (d.inf_key && cap <= d.inf_mask + 1) return;
-  const u64 oc = d.inf_key ? d.inf_mask + 1 : 0;
-  std::vector<i64> ok(oc), oc_(oc), op(oc);
-  std::vector<i32> og(oc);
-  std::vector<double> oa(oc);
-  std::vector<u64> orr(oc);
+  const u64 cap = pow2_at_least(std::max<u64>(4 * live + 64, 1024));
+  if (d.inf && cap <= d.inf_mask + 1) return;
+  const u64 oc = d.inf ? d.inf_mask + 1 : 0;
+  std::vector<InfRec> old(oc);
   if (oc) {
-    d2h(ok.data(), d.inf_key, oc * 8, h->stream);
-    d2h(og.data(), d.inf_gpu, oc * 4, h->stream);
-    d2h(oc_.data(), d.inf_cached, oc * 8, h->stream);
-    d2h(op.data(), d.inf_prompt, oc * 8, h->stream);
-    d2h(oa.data(), d.inf_arr, oc * 8, h->stream);
-    d2h(orr.data(), d.inf_root, oc * 8, h->stream);
+    d2h(old.data(), d.inf, oc * sizeof(InfRec), h->stream);
     ssync(h->stream);
   }
-  std::vector<i64> nk(cap, kNoInflight), nc(cap, 0), np(cap, 0);
-  std::vector<i32> ng(cap, 0);
-  std::vector<double> na(cap, 0);
-  std::vector<u64> nr(cap, 0);
+  InfRec empty;
+  memset(&empty, 0, sizeof(empty));
+  empty.key = kNoInflight;
+  std::vector<InfRec> nt(cap, empty);
   const u64 mask = cap - 1;
   for (u64 i = 0; i < oc; ++i) {
-    if (ok[i] == kNoInflight) continue;
-    u64 j = mix64((u64)ok[i]) & mask;
-    while (nk[j] != kNoInflight) j = (j + 1) & mask;
-    nk[j] = ok[i];
-    ng[j] = og[i];
-    nc[j] = oc_[i];
-    np[j] = op[i];
-    na[j] = oa[i];
-    nr[j] = orr[i];
+    if (old[i].key == kNoInflight) continue;
+    u64 j = mix64((u64)old[i].key) & mask;
+    while (nt[j].key != kNoInflight) j = (j + 1) & mask;
+    nt[j] = old[i];
   }
-  dfree(d.inf_key);
-  dfree(d.inf_gpu);
-  dfree(d.inf_cached);
-  dfree(d.inf_prompt);
-  dfree(d.inf_arr);
-  dfree(d.inf_root);
-  d.inf_key = talloc<i64>(cap);
-  d.inf_gpu = talloc<i32>(cap);
-  d.inf_cached = talloc<i64>(cap);
-  d.inf_prompt = talloc<i64>(cap);
-  d.inf_arr = talloc<double>(cap);
-  d.inf_root = talloc<u64>(cap);
-  h2d(d.inf_key, nk.data(), cap * 8, h->stream);
-  h2d(d.inf_gpu, ng.data(), cap * 4, h->stream);
-  h2d(d.inf_cached, nc.data(), cap * 8, h->stream);
-  h2d(d.inf_prompt, np.data(), cap * 8, h->stream);
-  h2d(d.inf_arr, na.data(), cap * 8, h->stream);
-  h2d(d.inf_root, nr.data(), cap * 8, h->stream);
+  dfree(d.inf);
+  d.inf = talloc<InfRec>(cap);
+  h2d(d.inf, nt.data(), cap * sizeof(InfRec), h->stream);
   ssync(h->stream);
   d.inf_mask = mask;
 }
@@ -610,6 +574,7 @@ void reserve_batch(e2_handle* h, i64 B) {
   dfree(h->b_o);
   dfree(h->b_dslot);
   dfree(h->b_dm);
+  dfree(h->b_path);
   dfree(h->b_state);
   dfree(h->b_A);
   dfree(h->b_B);
@@ -622,6 +587,7 @@ void reserve_batch(e2_handle* h, i64 B) {
   h->b_o = talloc<i64>(cap);
   h->b_dslot = talloc<u32>(cap);
   h->b_dm = talloc<u32>(cap);
+  h->b_path = talloc<u32>(cap * kPathHint);
   h->b_state = talloc<i32>(cap);
   h->b_A = talloc<u64>(cap);
   h->b_B = talloc<u64>(cap);
@@ -665,7 +631,7 @@ void reserve_for(e2_handle* h, i64 req, i64 toks) {
   reserve_nodes(h, (u64)h->hot.slots_used + 5 * (u64)req + 64);
   u64 maxw = 0, maxf = 0;
   for (int g = 0; g < h->G; ++g) {
-    maxw = std::max<u64>(maxw, h->hot.ws_tail[g] - h->hot.ws_head[g]);
+    maxw = std::max<u64>(maxw, h->hot.ws_tail[g] - h->hot.ws_done[g]);
     maxw = std::max<u64>(maxw, h->hot.wc_tail[g] - h->hot.wc_head[g]);
     maxf = std::max<u64>(maxf, h->hot.fifo_tail[g] - h->hot.fifo_head[g]);
   }
@@ -680,12 +646,27 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
     Timed t(h, a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER);
 #if E2_DEVICE_BUILD
     h->acc.launches[a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER]++;
-    k_serial<<<1, 32, 0, h->stream>>>(h->d, a);
+    k_serial<<<1, 32, h->serial_smem, h->stream>>>(h->d, a, h->nsets);
     CK(cudaGetLastError());
 #else
     Scr s;
     memset(&s, 0, sizeof(s));
-    serial_body(h->d, h->d.hot_g, &s, a);
+    const u32 ne = h->nsets * kWays;
+    std::vector<u32> tag(ne, kNil), tick(ne, 0), dirty(ne, 0);
+    std::vector<u64> data((size_t)ne * h->d.rs / 8);
+    NCache nc;
+    nc.nsets = h->nsets;
+    nc.clock = 0;
+    nc.victim = 0;
+    nc.tag = tag.data();
+    nc.tick = tick.data();
+    nc.dirty = dirty.data();
+    nc.data = (char*)data.data();
+    Ctx x;
+    x.d = h->d;
+    x.h = h->d.hot_g;
+    x.c = &nc;
+    serial_body(x, &s, a);
 #endif
   }
 }
@@ -702,7 +683,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
     unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
     h->acc.launches[E2_K_MATCH]++;
     k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(d, n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
-                                                             h->b_dm, h->d_bytes);
+                                                             h->b_dm, h->b_path, h->d_bytes);
     CK(cudaGetLastError());
   }
   h->acc.match_requests += n;
@@ -746,7 +727,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   std::vector<u32> ds(n), dm(n);
   for (i64 w = 0; w < n; ++w) {
     const i64 r = base + w;
-    MatchRes m = match_one(d, d.tok + h->r_off[r], h->r_len[r]);
+    MatchRes m = match_one(d, d.tok + h->r_off[r], h->r_len[r], h->b_path + w * kPathHint);
     S[w] = m.S;
     ds[w] = m.div_slot;
     dm[w] = m.div_m;
@@ -837,6 +818,7 @@ void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match) 
   a.kind = 1;
   a.op = op;
   a.out = h->d_api;
+  a.hint = need_match ? h->b_path : nullptr;
   push_hot(h);
   launch_serial(h, a);
   pull_hot(h);
@@ -881,7 +863,7 @@ void copy_decision(e2_handle* h, e2_decision* out, e2_cost* costs, double* ratio
 // Out of the hot path: it only fires after note_admitted fills the
 // queue statistics, which the trace driver never does.
 struct HostTree {
-  std::vector<NodeHdr> hdr;
+  std::vector<NodeRec> hdr;
   std::vector<u64> cmask, lamask;
   std::vector<double> la;
   std::vector<i32> hits;
@@ -897,11 +879,19 @@ void pull_tree(e2_handle* h, HostTree& t) {
   t.lamask.resize(n);
   t.la.resize(n * G);
   t.hits.resize(n * G);
-  d2h(t.hdr.data(), h->d.hdr, n * sizeof(NodeHdr), h->stream);
-  d2h(t.cmask.data(), h->d.cmask, n * 8, h->stream);
-  d2h(t.lamask.data(), h->d.lamask, n * 8, h->stream);
-  d2h(t.la.data(), h->d.la, n * G * 8, h->stream);
-  d2h(t.hits.data(), h->d.hits, n * G * 4, h->stream);
+  std::vector<char> raw(n * h->d.rs);
+  d2h(raw.data(), h->d.rec, raw.size(), h->stream);
+  ssync(h->stream);
+  for (u64 s = 0; s < n; ++s) {
+    NodeRec* r = (NodeRec*)(raw.data() + s * h->d.rs);
+    t.hdr[s] = *r;
+    t.cmask[s] = r->cmask;
+    t.lamask[s] = r->lamask;
+    for (int g = 0; g < G; ++g) {
+      t.la[s * G + g] = rla(r)[g];
+      t.hits[s * G + g] = rhits(r, G)[g];
+    }
+  }
   t.tok.resize(h->tok_len);
   d2h(t.tok.data(), h->tok, h->tok_len * 4, h->stream);
   ssync(h->stream);
@@ -1133,6 +1123,19 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     c.c3 = model->iteration_base_ms;
     zero_ptrs(h->d);
     h->d.cfg = c;
+    h->d.rs = rec_stride(n_gpus);
+    for (int g = 0; g < kMaxG; ++g) h->hot.ws_head_t[g] = h->hot.wc_head_t[g] = 1.0 / 0.0;
+    {
+      // node cache: as many 4-way sets as fit in ~150 KB of shared memory
+      u32 ne = 1;
+      while ((u64)(ne * 2) * (h->d.rs + 12) <= 150u * 1024 && ne * 2 <= 1024) ne *= 2;
+      h->nsets = std::max<u32>(ne / kWays, 1);
+      const u32 e = h->nsets * kWays;
+      h->serial_smem = ((3 * e * 4 + 15) / 16) * 16 + (size_t)e * h->d.rs;
+    }
+#if E2_DEVICE_BUILD
+    CK(cudaFuncSetAttribute(k_serial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->serial_smem));
+#endif
 #if E2_DEVICE_BUILD
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream_handle = h->stream;
@@ -1149,10 +1152,10 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     reserve_tokens(h, 1 << 16);
     reserve_requests(h, 1024);
     // root node: slot 0, id 0
-    NodeHdr root;
+    NodeRec root;
     memset(&root, 0, sizeof(root));
     root.parent = kNil;
-    h2d(h->d.hdr, &root, sizeof(root), h->stream);
+    h2d(h->d.rec, &root, sizeof(root), h->stream);
     push_hot(h);
     ssync(h->stream);
   });
@@ -1168,12 +1171,10 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
 void e2_destroy(e2_handle* h) {
   if (!h) return;
   Dev& d = h->d;
-  void* ptrs[] = {d.hdr, d.cmask, d.lamask, d.nchild, d.la, d.hits, d.ccc, d.ck, d.cv, d.ws_t, d.ws_missed, d.ws_est,
-                  d.ws_slot, d.wc_t, d.wc_out, d.dir_page, d.dir_la, d.dir_id, d.pg_la, d.pg_id, d.pg_slot, d.pg_n,
-                  d.free_pages, d.inf_key, d.inf_gpu, d.inf_cached, d.inf_prompt, d.inf_arr, d.inf_root, d.fifo_req,
-                  d.fifo_tail, d.scr_slot, d.scr_val, d.scr_la, d.scr_id, d.vic_slot, d.vic_tok, d.hot_g, h->tok,
-                  h->r_off, h->r_len, h->b_S, h->b_L, h->b_cand, h->b_leader, h->b_o, h->b_dslot, h->b_dm,
-                  h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api,
+  void* ptrs[] = {d.rec, d.ct, d.win, d.comp, d.dir, d.pg_la, d.pg_id, d.pg_slot, d.free_pages, d.inf, d.fifo_req,
+                  d.fifo_tail, d.req_tail, d.scr_slot, d.scr_val, d.scr_la, d.scr_id, d.vic_slot, d.vic_tok, d.hot_g,
+                  h->tok, h->r_off, h->r_len, h->b_S, h->b_L, h->b_cand, h->b_leader, h->b_o, h->b_dslot, h->b_dm,
+                  h->b_path, h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api,
                   h->st_ids, h->st_out, h->st_offs, h->st_arr, h->st_dec, h->st_cost, h->st_rat};
   for (void* p : ptrs) dfree(p);
 #if E2_DEVICE_BUILD
@@ -1194,25 +1195,32 @@ int e2_reset(e2_handle* h) {
     Dev& d = h->d;
     const int G = h->G;
     const u64 used = h->hot.slots_used;
-    dset(d.hdr, 0, used * sizeof(NodeHdr), h->stream);
-    dset(d.cmask, 0, used * 8, h->stream);
-    dset(d.lamask, 0, used * 8, h->stream);
-    dset(d.nchild, 0, used * 4, h->stream);
-    dset(d.la, 0, used * G * 8, h->stream);
-    dset(d.hits, 0, used * G * 4, h->stream);
-    dset(d.ccc, 0, used * G * 4, h->stream);
-    dset(d.ck, 0xff, (d.ct_mask + 1) * 8, h->stream);
-    dset(d.pg_n, 0, (size_t)h->hot.pages_used * 4, h->stream);
-    std::vector<i64> empty(d.inf_mask + 1, kNoInflight);
-    h2d(d.inf_key, empty.data(), empty.size() * 8, h->stream);
+    dset(d.rec, 0, used * d.rs, h->stream);
+    {
+      CtEntry e;
+      e.key = kEmptyKey;
+      e.val = 0;
+      e.pad = 0;
+      std::vector<CtEntry> empty_ct(d.ct_mask + 1, e);
+      h2d(d.ct, empty_ct.data(), empty_ct.size() * sizeof(CtEntry), h->stream);
+      InfRec z;
+      memset(&z, 0, sizeof(z));
+      z.key = kNoInflight;
+      std::vector<InfRec> empty_inf(d.inf_mask + 1, z);
+      h2d(d.inf, empty_inf.data(), empty_inf.size() * sizeof(InfRec), h->stream);
+      ssync(h->stream);
+    }
     memset(&h->hot, 0, sizeof(h->hot));
-    for (int g = 0; g < kMaxG; ++g) h->hot.redirect[g] = -1;
+    for (int g = 0; g < kMaxG; ++g) {
+      h->hot.redirect[g] = -1;
+      h->hot.ws_head_t[g] = h->hot.wc_head_t[g] = 1.0 / 0.0;
+    }
     h->hot.next_id = 1;
     h->hot.slots_used = 1;
-    NodeHdr root;
+    NodeRec root;
     memset(&root, 0, sizeof(root));
     root.parent = kNil;
-    h2d(d.hdr, &root, sizeof(root), h->stream);
+    h2d(d.rec, &root, sizeof(root), h->stream);
     push_hot(h);
     ssync(h->stream);
     h->tok_len = 0;
@@ -1463,7 +1471,7 @@ int e2_export(e2_handle* h, double now, e2_node* nodes, int32_t* tokens, double*
     i64 off = 0;
     for (size_t i = 0; i < order.size(); ++i) {
       const u32 x = order[i].first;
-      const NodeHdr& hd = t.hdr[x];
+      const NodeRec& hd = t.hdr[x];
       if (nodes) {
         nodes[i].id = hd.id;
         nodes[i].parent_id = x == kRoot ? hd.id : t.hdr[hd.parent].id;
@@ -1622,6 +1630,11 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     push_hot(h);
     const i64 B = drv->batch > 0 ? drv->batch : 16384;
     reserve_batch(h, std::min<i64>(B, n));
+    if (n > h->req_cap) {
+      dfree(h->d.req_tail);
+      h->d.req_tail = talloc<u32>(n);
+      h->req_cap = n;
+    }
     SerialArgs a;
     memset(&a, 0, sizeof(a));
     a.kind = 0;
@@ -1633,6 +1646,7 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     a.arr = d_arr;
     a.outl = d_out;
     a.L = h->b_L;
+    a.hint = h->b_path;
     a.dec = d_dec;
     a.costs = d_cost;
     a.ratios = d_rat;

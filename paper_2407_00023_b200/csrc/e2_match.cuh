@@ -57,28 +57,34 @@ struct MatchRes {
   i64 bytes;     // algorithmic bytes
 };
 
-// Warp-wide walk with token comparison.
-E2_D MatchRes match_one(const Dev& d, const i32* seq, i64 n) {
+// Warp-wide walk with token comparison; records up to kPathHint path slots.
+E2_D MatchRes match_one(const Dev& d, const i32* seq, i64 n, u32* path) {
   MatchRes r;
   r.S = 0;
   r.div_slot = kRoot;
   r.div_m = 0;
   i64 pos = 0, depth = 0;
   u32 cur = kRoot;
+  int level = 0;
   while (pos < n) {
-    u32 ch = child_lookup(d, cur, seq[pos]);
+    const u32 ch = child_lookup(d, cur, seq[pos]);
     depth++;
     if (ch == kNil) break;
-    const NodeHdr hd = d.hdr[ch];
-    const i64 lim = min_((i64)hd.edge_len, n - pos);
+    const NodeRec* hd = grec(d, ch);
+    const i64 off = hd->edge_off, len = hd->edge_len;
+    const i64 lim = min_(len, n - pos);
     // first token equal by construction of the child key
-    const i64 m = 1 + warp_lcp(d.tok + hd.edge_off + 1, seq + pos + 1, lim - 1);
+    const i64 m = 1 + warp_lcp(d.tok + off + 1, seq + pos + 1, lim - 1);
+    if (path && level < kPathHint && lane0()) path[level] = ch;
+    level++;
     pos += m;
     cur = ch;
     r.div_slot = ch;
     r.div_m = (u32)m;
-    if (m < (i64)hd.edge_len) break;
+    if (m < len) break;
   }
+  if (path && lane0())
+    for (int l = level; l < kPathHint; ++l) path[l] = kNil;
   r.S = pos;
   // B_match = 4*min(|p|, matched+1) + 4*matched + 32*(depth+1)
   r.bytes = 4 * min_(n, pos + 1) + 4 * pos + 32 * (depth + 1);

@@ -1,14 +1,16 @@
 // e2_state.cuh — HBM layout of one scheduler handle.
 //
 // Radix tree (reference: prefix_tree.hpp:20-39, prefix_tree.cpp):
-//   * node pool, slot-indexed SoA.  NodeHdr (32 B) is what a walk touches:
-//     creation id, edge = [edge_off, edge_off+edge_len) in the token arena,
-//     parent slot, first edge token, start depth.  Edges never copy tokens:
-//     they point into the arena that holds every prompt seen.
-//   * per-(slot, instance) arrays [slot*G + g]: last_access, windowed hit
-//     counter, cached-child count; per-slot 64-bit caching / last_access
-//     presence masks.
-//   * one global open-addressing child table keyed (parent_slot<<32 | token).
+//   * node pool of fixed-stride records (AoS): a 64-byte header (creation id,
+//     edge = [edge_off, edge_off+edge_len) in the token arena, parent slot,
+//     first edge token, start depth, caching / last_access-presence masks,
+//     child count) followed by per-instance last_access[G], windowed hit
+//     counters[G] and cached-child counts[G].  One record is one or a few
+//     coalesced warp loads; the serial kernel keeps hot records in a
+//     shared-memory cache (e2_tree.cuh).  Edges never copy tokens: they point
+//     into the arena that holds every prompt seen.
+//   * one global open-addressing child table keyed (parent_slot<<32 | token),
+//     16-byte entries so a 32-lane probe returns key and child together.
 //   * SPLIT KEEPS THE SLOT ON THE LOWER HALF: split_node (prefix_tree.cpp:
 //     122-154) gives the prefix the old id and the suffix a new id and the
 //     children.  Here the existing slot becomes the suffix (new id, keeps its
@@ -16,7 +18,8 @@
 //     id), so a split rewrites two table entries instead of rekeying every
 //     child, and any "node ending at depth d" slot stays valid forever.
 // Per-instance LRU index (prefix_tree.hpp:199-201): a paged ordered set of
-// (last_access bits, id) keys, 32 keys per page so one lane owns one key.
+// (last_access bits, id) keys, 32 keys per page so one lane owns one key; a
+// per-instance directory ring of 32-byte entries {page, count, max key}.
 // Load windows (cost_model.hpp:29-71): per-instance rings + integer sums.
 #pragma once
 
@@ -24,19 +27,73 @@
 
 namespace e2 {
 
-struct NodeHdr {
-  u64 id;        // creation order (reference NodeId)
-  i64 edge_off;  // token arena offset of the edge
-  u32 edge_len;  // 0 only for the root and for removed slots
-  u32 parent;    // slot, kNil for the root
-  i32 first_tok; // arena[edge_off]
-  u32 depth;     // tokens on the root path before this edge
+struct NodeRec {
+  u64 id;         // creation order (reference NodeId)
+  i64 edge_off;   // token arena offset of the edge
+  u32 edge_len;   // 0 only for the root and for removed slots
+  u32 parent;     // slot, kNil for the root
+  i32 first_tok;  // arena[edge_off]
+  u32 depth;      // tokens on the root path before this edge
+  u64 cmask;      // bit g: cached on instance g
+  u64 lamask;     // bit g: last_access[g] entry exists
+  i32 nchild;
+  i32 pad0;
+  u64 pad1;
+  // followed by: double la[G]; i32 hits[G]; i32 ccc[G];
+};
+static_assert(sizeof(NodeRec) == 64, "node header must stay 64 bytes");
+
+E2_HDX u32 rec_stride(int G) { return (u32)(((64 + 16 * G) + 127) / 128 * 128); }
+E2_HDX double* rla(NodeRec* r) { return (double*)((char*)r + 64); }
+E2_HDX i32* rhits(NodeRec* r, int G) { return (i32*)((char*)r + 64 + 8 * G); }
+E2_HDX i32* rccc(NodeRec* r, int G) { return (i32*)((char*)r + 64 + 12 * G); }
+E2_HDX const double* rla(const NodeRec* r) { return (const double*)((const char*)r + 64); }
+E2_HDX const i32* rhits(const NodeRec* r, int G) { return (const i32*)((const char*)r + 64 + 8 * G); }
+E2_HDX const i32* rccc(const NodeRec* r, int G) { return (const i32*)((const char*)r + 64 + 12 * G); }
+
+struct CtEntry {
+  u64 key;
+  u32 val;
+  u32 pad;
+};
+
+struct DirEntry {
+  u32 page;
+  i32 cnt;
+  u64 max_la;
+  u64 max_id;
+  u64 pad;
+};
+
+struct InfRec {
+  i64 key;
+  i32 gpu;
+  i32 pad;
+  i64 cached;
+  i64 prompt;
+  double arr;
+  u64 root;
+  u64 pad2;
+};
+
+struct WinEnt {
+  double t;
+  i64 missed;
+  i64 est;
+  u32 slot;
+  u32 pad;
+};
+
+struct CompEnt {
+  double t;
+  i64 out;
 };
 
 constexpr u64 kEmptyKey = ~0ull;
 constexpr u64 kTombKey = ~0ull - 1;
 constexpr i64 kNoInflight = INT64_MIN;
-constexpr int kPage = 32;  // LRU keys per page
+constexpr int kPage = 32;   // LRU keys per page
+constexpr int kPathHint = 8;  // path slots K1 records per request
 
 // Error codes mirrored from e2sched.h.
 constexpr i32 kErrConfig = 1;
@@ -92,8 +149,11 @@ struct Hot {
   i64 inflight_prompt[kMaxG];
   i32 redirect[kMaxG];
   u64 ws_head[kMaxG], ws_tail[kMaxG];
+  u64 ws_done[kMaxG];     // window entries whose hit stamps were already undone
+  double ws_head_t[kMaxG];  // time of the oldest scheduled entry
   i64 ws_missed_sum[kMaxG], ws_missed_nz[kMaxG];
   u64 wc_head[kMaxG], wc_tail[kMaxG];
+  double wc_head_t[kMaxG];
   i64 wc_output_sum[kMaxG];
   u32 dir_head[kMaxG], dir_n[kMaxG];
   u64 fifo_head[kMaxG], fifo_tail[kMaxG];
@@ -111,55 +171,38 @@ struct Hot {
   i64 err_req;  // request index / op index that failed
   i64 done;     // ops fully processed in the last launch
 };
+static_assert(sizeof(Hot) % 8 == 0, "Hot is copied as u64 words");
 
 struct Dev {
   Cfg cfg;
   const i32* tok;  // token arena
   // nodes
   u32 node_cap;
-  u32 pad1;
-  NodeHdr* hdr;
-  u64* cmask;
-  u64* lamask;
-  i32* nchild;
-  double* la;
-  i32* hits;
-  i32* ccc;
+  u32 rs;  // record stride (bytes)
+  char* rec;
   // child table
-  u64* ck;
-  u32* cv;
+  CtEntry* ct;
   u64 ct_mask;
   // windows
   u64 wcap;  // power of two per instance
-  double* ws_t;
-  i64* ws_missed;
-  i64* ws_est;
-  u32* ws_slot;
-  double* wc_t;
-  i64* wc_out;
+  WinEnt* win;
+  CompEnt* comp;
   // LRU
   u32 dcap;  // directory ring per instance (power of two)
   u32 page_cap;
-  u32* dir_page;
-  u64* dir_la;
-  u64* dir_id;
+  DirEntry* dir;
   u64* pg_la;
   u64* pg_id;
   u32* pg_slot;
-  i32* pg_n;
   u32* free_pages;
   // inflight map
   u64 inf_mask;
-  i64* inf_key;
-  i32* inf_gpu;
-  i64* inf_cached;
-  i64* inf_prompt;
-  double* inf_arr;
-  u64* inf_root;
-  // driver FIFO (criterion-7 eviction)
+  InfRec* inf;
+  // driver FIFO (criterion-7 eviction) and per-request tail slots
   u64 fcap;
   i64* fifo_req;
   i64* fifo_tail;
+  u32* req_tail;  // replay: node ending at |p_r| after request r's commit
   // scratch: per instance plan work lists, serial victim list
   u32 scap;
   u32 vcap;
@@ -171,5 +214,7 @@ struct Dev {
   i64* vic_tok;
   Hot* hot_g;
 };
+
+E2_HDX NodeRec* grec(const Dev& d, u32 s) { return (NodeRec*)(d.rec + (u64)s * d.rs); }
 
 }  // namespace e2
