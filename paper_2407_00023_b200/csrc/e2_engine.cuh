@@ -37,59 +37,59 @@ struct Walk {
 // ---------------------------------------------------------------------------
 // Load windows — LoadWindow (cost_model.cpp:20-73).  Single-lane.
 // ---------------------------------------------------------------------------
-E2_HD u64 wslot(const Dev& d, int g, u64 i) { return (u64)g * d.wcap + (i & (d.wcap - 1)); }
+E2_HD u64 wslot(int g, u64 i) { return (u64)g * DEV.wcap + (i & (DEV.wcap - 1)); }
 
 constexpr double kInf = __builtin_huge_val();
 
 // prune (cost_model.cpp:31-42): inclusive horizon, t >= now - H survives.
 // Hit stamps of pruned entries are undone lazily (hits_catchup).
-E2_HD void win_prune(const Dev& d, Hot* h, int g, double now) {
-  const double cutoff = dsub(now, d.cfg.H);
-  if (h->ws_head_t[g] < cutoff) {
-    u64 hd = h->ws_head[g];
-    const u64 tl = h->ws_tail[g];
-    double t = h->ws_head_t[g];
+E2_HD void win_prune(int g, double now) {
+  const double cutoff = dsub(now, DEV.cfg.H);
+  if (HOT.ws_head_t[g] < cutoff) {
+    u64 hd = HOT.ws_head[g];
+    const u64 tl = HOT.ws_tail[g];
+    double t = HOT.ws_head_t[g];
     while (hd < tl && t < cutoff) {
-      const i64 m = d.win[wslot(d, g, hd)].missed;
-      h->ws_missed_sum[g] -= m;
-      if (m > 0) h->ws_missed_nz[g] -= 1;
+      const i64 m = DEV.win[wslot(g, hd)].missed;
+      HOT.ws_missed_sum[g] -= m;
+      if (m > 0) HOT.ws_missed_nz[g] -= 1;
       hd++;
-      t = hd < tl ? d.win[wslot(d, g, hd)].t : kInf;
+      t = hd < tl ? DEV.win[wslot(g, hd)].t : kInf;
     }
-    h->ws_head[g] = hd;
-    h->ws_head_t[g] = t;
+    HOT.ws_head[g] = hd;
+    HOT.ws_head_t[g] = t;
   }
-  if (h->wc_head_t[g] < cutoff) {
-    u64 ch = h->wc_head[g];
-    const u64 ct = h->wc_tail[g];
-    double t = h->wc_head_t[g];
+  if (HOT.wc_head_t[g] < cutoff) {
+    u64 ch = HOT.wc_head[g];
+    const u64 ct = HOT.wc_tail[g];
+    double t = HOT.wc_head_t[g];
     while (ch < ct && t < cutoff) {
-      h->wc_output_sum[g] -= d.comp[wslot(d, g, ch)].out;
+      HOT.wc_output_sum[g] -= DEV.comp[wslot(g, ch)].out;
       ch++;
-      t = ch < ct ? d.comp[wslot(d, g, ch)].t : kInf;
+      t = ch < ct ? DEV.comp[wslot(g, ch)].t : kInf;
     }
-    h->wc_head[g] = ch;
-    h->wc_head_t[g] = t;
+    HOT.wc_head[g] = ch;
+    HOT.wc_head_t[g] = t;
   }
 }
 
 // load_ms (cost_model.cpp:65-73) — prefill folded from integer sums, decode
 // = count * (c2 * avg_output).
-E2_HD double win_load(const Dev& d, Hot* h, int g, double now) {
-  win_prune(d, h, g, now);
-  const Cfg& c = d.cfg;
-  const i64 nsched = (i64)(h->ws_tail[g] - h->ws_head[g]);
-  const i64 ncomp = (i64)(h->wc_tail[g] - h->wc_head[g]);
-  const double prefill = dadd(dmul(c.c0, i2d(h->ws_missed_nz[g])), dmul(c.c1, i2d(h->ws_missed_sum[g])));
-  const double avg = ncomp == 0 ? i2d(c.default_out) : ddiv(i2d(h->wc_output_sum[g]), i2d(ncomp));
+E2_HD double win_load(int g, double now) {
+  win_prune(g, now);
+  const Cfg& c = DEV.cfg;
+  const i64 nsched = (i64)(HOT.ws_tail[g] - HOT.ws_head[g]);
+  const i64 ncomp = (i64)(HOT.wc_tail[g] - HOT.wc_head[g]);
+  const double prefill = dadd(dmul(c.c0, i2d(HOT.ws_missed_nz[g])), dmul(c.c1, i2d(HOT.ws_missed_sum[g])));
+  const double avg = ncomp == 0 ? i2d(c.default_out) : ddiv(i2d(HOT.wc_output_sum[g]), i2d(ncomp));
   const double decode = dmul(i2d(nsched), dmul(c.c2, avg));
   return dadd(prefill, decode);
 }
 
-E2_HD bool win_add_sched(const Dev& d, Hot* h, int g, double now, i64 missed, i64 est, u32 tail) {
-  const u64 t = h->ws_tail[g];
-  if (t - h->ws_done[g] >= d.wcap) {
-    set_err(h, kErrCapacity, kWhyWindowCap);
+E2_HD bool win_add_sched(int g, double now, i64 missed, i64 est, u32 tail) {
+  const u64 t = HOT.ws_tail[g];
+  if (t - HOT.ws_done[g] >= DEV.wcap) {
+    set_err(kErrCapacity, kWhyWindowCap);
     return false;
   }
   WinEnt e;
@@ -98,27 +98,27 @@ E2_HD bool win_add_sched(const Dev& d, Hot* h, int g, double now, i64 missed, i6
   e.est = est;
   e.slot = tail;
   e.pad = 0;
-  d.win[wslot(d, g, t)] = e;
-  if (t == h->ws_head[g]) h->ws_head_t[g] = now;
-  h->ws_tail[g] = t + 1;
-  h->ws_missed_sum[g] += missed;
-  if (missed > 0) h->ws_missed_nz[g] += 1;
+  DEV.win[wslot(g, t)] = e;
+  if (t == HOT.ws_head[g]) HOT.ws_head_t[g] = now;
+  HOT.ws_tail[g] = t + 1;
+  HOT.ws_missed_sum[g] += missed;
+  if (missed > 0) HOT.ws_missed_nz[g] += 1;
   return true;
 }
 
-E2_HD bool win_add_comp(const Dev& d, Hot* h, int g, double now, i64 out) {
-  const u64 t = h->wc_tail[g];
-  if (t - h->wc_head[g] >= d.wcap) {
-    set_err(h, kErrCapacity, kWhyWindowCap);
+E2_HD bool win_add_comp(int g, double now, i64 out) {
+  const u64 t = HOT.wc_tail[g];
+  if (t - HOT.wc_head[g] >= DEV.wcap) {
+    set_err(kErrCapacity, kWhyWindowCap);
     return false;
   }
   CompEnt e;
   e.t = now;
   e.out = out;
-  d.comp[wslot(d, g, t)] = e;
-  if (t == h->wc_head[g]) h->wc_head_t[g] = now;
-  h->wc_tail[g] = t + 1;
-  h->wc_output_sum[g] += out;
+  DEV.comp[wslot(g, t)] = e;
+  if (t == HOT.wc_head[g]) HOT.wc_head_t[g] = now;
+  HOT.wc_tail[g] = t + 1;
+  HOT.wc_output_sum[g] += out;
   return true;
 }
 
@@ -127,23 +127,21 @@ E2_HD bool win_add_comp(const Dev& d, Hot* h, int g, double now, i64 out) {
 // window since the last catch-up, walking each one's path from its tail
 // slot (splits since then put the copied stamps on the new prefix nodes,
 // which the parent walk visits too).  Warp-wide.
-E2_D void hits_catchup(Ctx& x, int g) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
-  const int G = d.cfg.G;
-  while (h->ws_done[g] < h->ws_head[g]) {
-    const u32 tail = d.win[wslot(d, g, h->ws_done[g])].slot;
+E2_DNI void hits_catchup(int g) {
+  const int G = DEV.cfg.G;
+  while (HOT.ws_done[g] < HOT.ws_head[g]) {
+    const u32 tail = DEV.win[wslot(g, HOT.ws_done[g])].slot;
     for (u32 n = tail; n != kRoot && n != kNil;) {
-      NodeRec* r = nget(x, n);
+      NodeRec* r = nget(n);
       const u32 p = r->parent;
       if (lane0()) {
         rhits(r, G)[g] -= 1;
-        ndirty(x, r);
+        ndirty(r);
       }
       wsync();
       n = p;
     }
-    if (lane0()) h->ws_done[g]++;
+    if (lane0()) HOT.ws_done[g]++;
     wsync();
   }
 }
@@ -161,22 +159,20 @@ E2_HD double prefill_time(const Cfg& c, i64 missed) {
 // Returns freed tokens.
 // ---------------------------------------------------------------------------
 template <typename Visit>
-E2_HD i64 plan_eviction(const Ctx& x, int g, i64 need, bool partial, Visit&& visit) {
+E2_HD i64 plan_eviction(int g, i64 need, bool partial, Visit&& visit) {
   if (need <= 0) return 0;
-  const Dev& d = x.d;
-  Hot* h = x.h;
-  const int G = d.cfg.G;
-  const u32 half = d.scap / 2;
-  u32* s_slot = d.scr_slot + (u64)g * d.scap;  // [0,half): surfaced list, [half,scap): sim ccc
-  u64* s_la = d.scr_la + (u64)g * d.scap;
-  u64* s_id = d.scr_id + (u64)g * d.scap;
-  i64* s_val = d.scr_val + (u64)g * d.scap;
+  const int G = DEV.cfg.G;
+  const u32 half = DEV.scap / 2;
+  u32* s_slot = DEV.scr_slot + (u64)g * DEV.scap;  // [0,half): surfaced list, [half,scap): sim ccc
+  u64* s_la = DEV.scr_la + (u64)g * DEV.scap;
+  u64* s_id = DEV.scr_id + (u64)g * DEV.scap;
+  i64* s_val = DEV.scr_val + (u64)g * DEV.scap;
   u32 ns = 0, nsurf_head = 0, nsim = 0;
-  const u32 nd = h->dir_n[g];
+  const u32 nd = HOT.dir_n[g];
   u32 k = 0, j = 0, page = kNil;
   i32 pcnt = 0;
   if (nd > 0) {
-    const DirEntry e = d.dir[dring(d, h, g, 0)];
+    const DirEntry e = DEV.dir[dring(g, 0)];
     page = e.page;
     pcnt = e.cnt;
   }
@@ -189,18 +185,18 @@ E2_HD i64 plan_eviction(const Ctx& x, int g, i64 need, bool partial, Visit&& vis
     bool take_b = false;
     if (have_a && have_b) {
       const u64 ai = (u64)page * kPage + j;
-      take_b = kless(s_la[nsurf_head], s_id[nsurf_head], d.pg_la[ai], d.pg_id[ai]);
+      take_b = kless(s_la[nsurf_head], s_id[nsurf_head], DEV.pg_la[ai], DEV.pg_id[ai]);
     } else {
       take_b = have_b;
     }
     if (take_b) {
       v = s_slot[nsurf_head++];
     } else {
-      v = d.pg_slot[(u64)page * kPage + j];
+      v = DEV.pg_slot[(u64)page * kPage + j];
       if (++j >= (u32)pcnt) {
         j = 0;
         if (++k < nd) {
-          const DirEntry e = d.dir[dring(d, h, g, k)];
+          const DirEntry e = DEV.dir[dring(g, k)];
           page = e.page;
           pcnt = e.cnt;
         } else {
@@ -208,7 +204,7 @@ E2_HD i64 plan_eviction(const Ctx& x, int g, i64 need, bool partial, Visit&& vis
         }
       }
     }
-    const NodeRec* rv = npeek(x, v);
+    const NodeRec* rv = npeek(v);
     const i64 tok = rv->edge_len;
     const i64 remaining = need - freed;
     if (partial && tok > remaining) {
@@ -220,7 +216,7 @@ E2_HD i64 plan_eviction(const Ctx& x, int g, i64 need, bool partial, Visit&& vis
     freed += tok;
     const u32 p = rv->parent;
     if (p != kNil && p != kRoot) {
-      const NodeRec* rp = npeek(x, p);
+      const NodeRec* rp = npeek(p);
       if (!rcached(rp, g)) continue;
       u32 xi = 0;
       while (xi < nsim && s_slot[half + xi] != p) ++xi;
@@ -228,8 +224,8 @@ E2_HD i64 plan_eviction(const Ctx& x, int g, i64 need, bool partial, Visit&& vis
       if (xi < nsim) {
         c = s_val[half + xi] - 1;
       } else {
-        if (nsim >= d.scap - half) {
-          set_err(h, kErrCapacity, kWhyScratchCap);
+        if (nsim >= DEV.scap - half) {
+          set_err(kErrCapacity, kWhyScratchCap);
           break;
         }
         c = (i64)rccc(rp, G)[g] - 1;
@@ -240,7 +236,7 @@ E2_HD i64 plan_eviction(const Ctx& x, int g, i64 need, bool partial, Visit&& vis
       if (c == 0) {
         // sorted insert into the pending part of the surfaced list
         if (ns >= half) {
-          set_err(h, kErrCapacity, kWhyScratchCap);
+          set_err(kErrCapacity, kWhyScratchCap);
           break;
         }
         const u64 pla = dbits(rla(rp)[g]), pid = rp->id;
@@ -268,22 +264,20 @@ struct CostOut {
   bool inf;
 };
 
-E2_HD CostOut cost_for(const Ctx& x, int g, i64 missed, double now) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
+E2_HD CostOut cost_for(int g, i64 missed, double now) {
   CostOut o;
-  o.L = win_load(d, h, g, now);
-  o.P = prefill_time(d.cfg, missed);
+  o.L = win_load(g, now);
+  o.P = prefill_time(DEV.cfg, missed);
   o.M = 0.0;
   o.inf = false;
-  const i64 free_tokens = d.cfg.cap - h->cached_tokens[g];
+  const i64 free_tokens = DEV.cfg.cap - HOT.cached_tokens[g];
   const i64 need = missed - free_tokens;
   if (need > 0) {
-    const i64 total = (i64)(h->ws_tail[g] - h->ws_head[g]);  // scheduled_count (already pruned)
-    const Cfg& c = d.cfg;
+    const i64 total = (i64)(HOT.ws_tail[g] - HOT.ws_head[g]);  // scheduled_count (already pruned)
+    const Cfg& c = DEV.cfg;
     const int G = c.G;
     double M = 0.0;
-    const i64 freed = plan_eviction(x, g, need, false, [&](u32, i64 tok, const NodeRec* rv) {
+    const i64 freed = plan_eviction(g, need, false, [&](u32, i64 tok, const NodeRec* rv) {
       if (total > 0) {
         const double nj = ddiv(i2d(rhits(rv, G)[g]), i2d(total));
         M = dadd(M, dmul(prefill_time(c, tok), nj));
@@ -297,10 +291,10 @@ E2_HD CostOut cost_for(const Ctx& x, int g, i64 missed, double now) {
 
 // Warp-wide: make g's windowed hit counters current before a cost with an
 // eviction term is evaluated.
-E2_D void cost_prepare(Ctx& x, int g, i64 missed, double now) {
-  if (lane0()) win_prune(x.d, x.h, g, now);
+E2_DNI void cost_prepare(int g, i64 missed, double now) {
+  if (lane0()) win_prune(g, now);
   wsync();
-  if (missed - (x.d.cfg.cap - x.h->cached_tokens[g]) > 0) hits_catchup(x, g);
+  if (missed - (DEV.cfg.cap - HOT.cached_tokens[g]) > 0) hits_catchup(g);
 }
 
 // ---------------------------------------------------------------------------
@@ -308,15 +302,14 @@ E2_D void cost_prepare(Ctx& x, int g, i64 missed, double now) {
 // current tree, from the batched match; prefix_tree.cpp:79-114.  `hint`
 // holds K1's path slots (may be stale after in-batch splits; validated).
 // ---------------------------------------------------------------------------
-E2_D Walk walk_known(Ctx& x, const i32* seq, i64 L, const u32* hint, int nhint, i64* ext) {
-  const Dev& d = x.d;
+E2_DNI Walk walk_known(const i32* seq, i64 L, const u32* hint, int nhint, i64* ext) {
   Walk w;
   w.last = kRoot;
   w.last_m = 0;
   w.cached_len = 0;
   w.present = 0;
   w.ok = true;
-  const int G = d.cfg.G;
+  const int G = DEV.cfg.G;
   for (int g = lane(); g < G; g += kWidth) ext[g] = 0;
   u64 alive = 0;
   bool first_span = true;
@@ -329,16 +322,16 @@ E2_D Walk walk_known(Ctx& x, const i32* seq, i64 L, const u32* hint, int nhint, 
     if (level < nhint) {
       const u32 c = hint[level];
       if (c != kNil) {
-        const NodeRec* rc = nget(x, c);
+        const NodeRec* rc = nget(c);
         if (rc->parent == cur && rc->first_tok == t && rc->edge_len > 0) ch = c;
       }
     }
-    if (ch == kNil) ch = child_lookup(d, cur, t);
+    if (ch == kNil) ch = child_lookup(cur, t);
     if (ch == kNil) {
       w.ok = false;
       break;
     }
-    const NodeRec* r = nget(x, ch);
+    const NodeRec* r = nget(ch);
     const i64 len = r->edge_len;
     const i64 m = min_(len, L - pos);
     const u64 cm = r->cmask;
@@ -365,30 +358,28 @@ E2_D Walk walk_known(Ctx& x, const i32* seq, i64 L, const u32* hint, int nhint, 
 
 // ensure_path (prefix_tree.cpp:156-185) given the walk of the same sequence.
 // Returns the node whose edge ends exactly at |seq| (kNil on error).
-E2_D u32 ensure_path(Ctx& x, i64 seq_off, i64 n, i64 L, const Walk& w) {
+E2_DNI u32 ensure_path(i64 seq_off, i64 n, i64 L, const Walk& w) {
   u32 cur = (L == 0) ? kRoot : w.last;
-  if (L > 0 && w.last_m < (i64)nget(x, w.last)->edge_len) {
-    cur = split_node(x, w.last, (u32)w.last_m);
+  if (L > 0 && w.last_m < (i64)nget(w.last)->edge_len) {
+    cur = split_node(w.last, (u32)w.last_m);
     if (cur == kNil) return kNil;
   }
   if (L == n) return cur;
-  return new_leaf(x, cur, seq_off + L, (u32)(n - L), (u32)L);
+  return new_leaf(cur, seq_off + L, (u32)(n - L), (u32)L);
 }
 
 // ---------------------------------------------------------------------------
 // Redirect upkeep — update_redirects (global_scheduler.cpp:194-219).  Warp-wide.
 // ---------------------------------------------------------------------------
-E2_D void update_redirects(Ctx& x, Scr* s, double now) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
-  const int G = d.cfg.G;
-  for (int g = lane(); g < G; g += kWidth) s->loads[g] = win_load(d, h, g, now);
+E2_DNI void update_redirects(Scr* s, double now) {
+  const int G = DEV.cfg.G;
+  for (int g = lane(); g < G; g += kWidth) s->loads[g] = win_load(g, now);
   wsync();
   if (lane0()) {
-    const double th = d.cfg.th_bal;
+    const double th = DEV.cfg.th_bal;
     for (int src = 0; src < G; ++src) {
-      const int dst = h->redirect[src];
-      if (dst >= 0 && s->loads[src] <= dmul(th, s->loads[dst])) h->redirect[src] = -1;
+      const int dst = HOT.redirect[src];
+      if (dst >= 0 && s->loads[src] <= dmul(th, s->loads[dst])) HOT.redirect[src] = -1;
     }
     int hi = 0, lo = 0;
     for (int g = 1; g < G; ++g) {
@@ -396,9 +387,9 @@ E2_D void update_redirects(Ctx& x, Scr* s, double now) {
       if (s->loads[g] < s->loads[lo]) lo = g;
     }
     if (!(hi == lo || !(s->loads[hi] > dmul(th, s->loads[lo])))) {
-      if (h->redirect[hi] != lo) {
-        h->redirect[hi] = lo;
-        h->stats[kStInstalls]++;
+      if (HOT.redirect[hi] != lo) {
+        HOT.redirect[hi] = lo;
+        HOT.stats[kStInstalls]++;
       }
     }
   }
@@ -445,9 +436,7 @@ E2_HD void put_cost(Scr* s, int idx, int g, const CostOut& c) {
 
 // decide (global_scheduler.cpp:76-158).  Warp-wide.  Fills s->c* and
 // s->ratios; w receives the walk for a following commit.
-E2_D Dec decide(Ctx& x, Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, double now, Walk& w) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
+E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, double now, Walk& w) {
   Dec r;
   r.branch = 1;
   r.gpu = -1;
@@ -459,28 +448,28 @@ E2_D Dec decide(Ctx& x, Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, i
   r.matched = L;
   r.has_ratios = 0;
   r.ok = 1;
-  const int G = d.cfg.G;
+  const int G = DEV.cfg.G;
   if (lane0()) s->n_costs = 0;
   wsync();
-  if (n > d.cfg.cap) {
-    if (lane0()) set_err(h, kErrNoAdmissible, kWhyPromptTooLong);
+  if (n > DEV.cfg.cap) {
+    if (lane0()) set_err(kErrNoAdmissible, kWhyPromptTooLong);
     wsync();
     r.ok = 0;
     return r;
   }
-  if (d.cfg.mode == 1) {
+  if (DEV.cfg.mode == 1) {
     r.branch = 3;
-    r.gpu = (i32)(h->rr_next % G);
+    r.gpu = (i32)(HOT.rr_next % G);
     r.missed_len = n;
     r.moc = n;
     r.matched = 0;
     return r;
   }
-  if (lane0()) h->stats[kStTreeReads]++;
+  if (lane0()) HOT.stats[kStTreeReads]++;
   wsync();
-  w = walk_known(x, seq, L, hint, nhint, s->ext);
+  w = walk_known(seq, L, hint, nhint, s->ext);
   if (!w.ok) {
-    if (lane0()) set_err(h, kErrSim, kWhyWalk);
+    if (lane0()) set_err(kErrSim, kWhyWalk);
     wsync();
     r.ok = 0;
     return r;
@@ -502,25 +491,25 @@ E2_D Dec decide(Ctx& x, Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, i
     }
     for (u64 m = cand; m; m &= m - 1) {
       const int g = ffs64(m);
-      cost_prepare(x, g, n - s->ext[g], now);
+      cost_prepare(g, n - s->ext[g], now);
     }
     for (int g = lane(); g < G; g += kWidth) {
       if ((cand >> g) & 1ull) {
         const int idx = popc64(cand & ((1ull << g) - 1));
-        put_cost(s, idx, g, cost_for(x, g, n - s->ext[g], now));
+        put_cost(s, idx, g, cost_for(g, n - s->ext[g], now));
       }
     }
     wsync();
     int nc = popc64(cand);
     int gpu = pick_min(s, nc);
-    if (gpu >= 0 && h->redirect[gpu] >= 0 && h->redirect[gpu] != gpu) {
-      const int t = h->redirect[gpu];
+    if (gpu >= 0 && HOT.redirect[gpu] >= 0 && HOT.redirect[gpu] != gpu) {
+      const int t = HOT.redirect[gpu];
       int ti = -1;
       for (int i = 0; i < nc; ++i)
         if (s->cgpu[i] == t) ti = i;
       if (ti < 0) {
-        cost_prepare(x, t, n - s->ext[t], now);
-        if (lane0()) put_cost(s, nc, t, cost_for(x, t, n - s->ext[t], now));
+        cost_prepare(t, n - s->ext[t], now);
+        if (lane0()) put_cost(s, nc, t, cost_for(t, n - s->ext[t], now));
         wsync();
         ti = nc;
         nc++;
@@ -537,8 +526,8 @@ E2_D Dec decide(Ctx& x, Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, i
   } else {
     r.has_ratios = 1;
     for (int g = lane(); g < G; g += kWidth) {
-      const i64 ip = h->inflight_prompt[g];
-      s->ratios[g] = ip <= 0 ? 0.0 : ddiv(i2d(h->inflight_cached[g]), i2d(ip));
+      const i64 ip = HOT.inflight_prompt[g];
+      s->ratios[g] = ip <= 0 ? 0.0 : ddiv(i2d(HOT.inflight_cached[g]), i2d(ip));
     }
     wsync();
     int max_g = -1;
@@ -549,25 +538,25 @@ E2_D Dec decide(Ctx& x, Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, i
         max_g = g;
       }
     }
-    if (d.cfg.pd_balance && max_r > d.cfg.imbal) {
+    if (DEV.cfg.pd_balance && max_r > DEV.cfg.imbal) {
       r.branch = 2;
       r.gpu = max_g;
     } else {
       r.branch = 1;
-      for (int g = 0; g < G; ++g) cost_prepare(x, g, n - s->ext[g], now);
-      for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(x, g, n - s->ext[g], now));
+      for (int g = 0; g < G; ++g) cost_prepare(g, n - s->ext[g], now);
+      for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(g, n - s->ext[g], now));
       wsync();
       if (lane0()) s->n_costs = G;
       wsync();
       r.gpu = pick_min(s, G);
     }
   }
-  if (h->err) {
+  if (HOT.err) {
     r.ok = 0;
     return r;
   }
   if (r.gpu < 0 || r.gpu >= G) {
-    if (lane0()) set_err(h, kErrSim, kWhyNotContiguous);
+    if (lane0()) set_err(kErrSim, kWhyNotContiguous);
     wsync();
     r.ok = 0;
     return r;
@@ -580,10 +569,10 @@ E2_D Dec decide(Ctx& x, Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, i
 // Inflight map: request id -> placement (global_scheduler.hpp:129-135).
 // Single-lane; linear probing with backward-shift deletion; 64-byte records.
 // ---------------------------------------------------------------------------
-E2_HD u64 inf_find(const Dev& d, i64 id, bool& found) {
-  u64 i = mix64((u64)id) & d.inf_mask;
-  for (u64 k = 0; k <= d.inf_mask; ++k, i = (i + 1) & d.inf_mask) {
-    const i64 key = d.inf[i].key;
+E2_HD u64 inf_find(i64 id, bool& found) {
+  u64 i = mix64((u64)id) & DEV.inf_mask;
+  for (u64 k = 0; k <= DEV.inf_mask; ++k, i = (i + 1) & DEV.inf_mask) {
+    const i64 key = DEV.inf[i].key;
     if (key == kNoInflight) {
       found = false;
       return i;
@@ -597,68 +586,66 @@ E2_HD u64 inf_find(const Dev& d, i64 id, bool& found) {
   return ~0ull;
 }
 
-E2_HD void inf_erase_at(const Dev& d, u64 i) {
+E2_HD void inf_erase_at(u64 i) {
   u64 j = i;
   for (;;) {
-    j = (j + 1) & d.inf_mask;
-    const InfRec rj = d.inf[j];
+    j = (j + 1) & DEV.inf_mask;
+    const InfRec rj = DEV.inf[j];
     if (rj.key == kNoInflight) break;
-    const u64 home = mix64((u64)rj.key) & d.inf_mask;
+    const u64 home = mix64((u64)rj.key) & DEV.inf_mask;
     // move j into the hole at i if home is not cyclically in (i, j]
     const bool in_range = (i <= j) ? (home > i && home <= j) : (home > i || home <= j);
     if (!in_range) {
-      d.inf[i] = rj;
+      DEV.inf[i] = rj;
       i = j;
     }
   }
-  d.inf[i].key = kNoInflight;
+  DEV.inf[i].key = kNoInflight;
 }
 
 // commit (global_scheduler.cpp:160-175).  Warp-wide.  Returns the tail slot.
-E2_D u32 commit(Ctx& x, i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
+E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
                 double now) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
-  if (d.cfg.mode == 1) {
-    if (lane0()) h->rr_next++;
+  if (DEV.cfg.mode == 1) {
+    if (lane0()) HOT.rr_next++;
     wsync();
     return kNil;
   }
   if (n == 0) {
-    if (lane0()) set_err(h, kErrSim, kWhyEmptyInsert);
+    if (lane0()) set_err(kErrSim, kWhyEmptyInsert);
     wsync();
     return kNil;
   }
-  const u32 tail = ensure_path(x, seq_off, n, L, w);
-  if (tail == kNil || h->err) return kNil;
+  const u32 tail = ensure_path(seq_off, n, L, w);
+  if (tail == kNil || HOT.err) return kNil;
   const int g = r.gpu;
-  const int G = d.cfg.G;
+  const int G = DEV.cfg.G;
   // record_hit bottom-up (prefix_tree.cpp:193-196)
   u64 root_id = 0;
   for (u32 v = tail; v != kRoot;) {
-    NodeRec* rv = nget(x, v);
+    NodeRec* rv = nget(v);
     const u32 p = rv->parent;
     root_id = rv->id;
     if (lane0()) {
       rhits(rv, G)[g] += 1;
-      ndirty(x, rv);
+      ndirty(rv);
     }
     wsync();
-    touch_la(x, v, g, now);
+    touch_la(v, g, now);
     v = p;
   }
   if (lane0()) {
-    win_add_sched(d, h, g, now, r.moc, d.cfg.default_out, tail);
-    h->inflight_cached[g] += r.cached_len;
-    h->inflight_prompt[g] += n;
+    win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail);
+    HOT.inflight_cached[g] += r.cached_len;
+    HOT.inflight_prompt[g] += n;
     bool found;
-    const u64 i = inf_find(d, req_id, found);
+    const u64 i = inf_find(req_id, found);
     if (i == ~0ull) {
-      set_err(h, kErrCapacity, kWhyInflightCap);
+      set_err(kErrCapacity, kWhyInflightCap);
     } else {
       if (!found) {
-        h->inflight_n++;
-        if ((u64)h->inflight_n * 2 > d.inf_mask + 1) set_err(h, kErrCapacity, kWhyInflightCap);
+        HOT.inflight_n++;
+        if ((u64)HOT.inflight_n * 2 > DEV.inf_mask + 1) set_err(kErrCapacity, kWhyInflightCap);
       }
       InfRec e;
       e.key = req_id;
@@ -669,7 +656,7 @@ E2_D u32 commit(Ctx& x, i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, 
       e.arr = arrival;
       e.root = root_id;
       e.pad2 = 0;
-      d.inf[i] = e;
+      DEV.inf[i] = e;
     }
   }
   wsync();
@@ -677,37 +664,35 @@ E2_D u32 commit(Ctx& x, i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, 
 }
 
 // Stats (global_scheduler.cpp:183-189).
-E2_D void count_stats(Hot* h, const Dec& r) {
+E2_D void count_stats(const Dec& r) {
   if (lane0()) {
-    h->stats[r.branch == 0 ? kStExploit : r.branch == 1 ? kStExplore : r.branch == 2 ? kStPressure : kStRoundRobin]++;
-    if (r.redirected) h->stats[kStRedirected]++;
+    HOT.stats[r.branch == 0 ? kStExploit : r.branch == 1 ? kStExplore : r.branch == 2 ? kStPressure : kStRoundRobin]++;
+    if (r.redirected) HOT.stats[kStRedirected]++;
   }
   wsync();
 }
 
 // mark_cached_path bottom-up part (prefix_tree.cpp:203-211) from a known tail.
-E2_D void mark_cached_chain(Ctx& x, u32 tail, int g, double now) {
+E2_DNI void mark_cached_chain(u32 tail, int g, double now) {
   for (u32 v = tail; v != kRoot;) {
-    set_cached(x, v, g);
-    touch_la(x, v, g, now);
-    v = nget(x, v)->parent;
+    set_cached(v, g);
+    touch_la(v, g, now);
+    v = nget(v)->parent;
   }
 }
 
 // note_finished (global_scheduler.cpp:361-369).  Warp-wide.
-E2_D void note_finished(Ctx& x, i64 id, double now, i64 out) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
+E2_DNI void note_finished(i64 id, double now, i64 out) {
   if (lane0()) {
     bool found;
-    const u64 i = inf_find(d, id, found);
+    const u64 i = inf_find(id, found);
     if (found) {
-      const InfRec e = d.inf[i];
-      win_add_comp(d, h, e.gpu, now, out);
-      h->inflight_cached[e.gpu] -= e.cached;
-      h->inflight_prompt[e.gpu] -= e.prompt;
-      inf_erase_at(d, i);
-      h->inflight_n--;
+      const InfRec e = DEV.inf[i];
+      win_add_comp(e.gpu, now, out);
+      HOT.inflight_cached[e.gpu] -= e.cached;
+      HOT.inflight_prompt[e.gpu] -= e.prompt;
+      inf_erase_at(i);
+      HOT.inflight_n--;
     }
   }
   wsync();
@@ -716,16 +701,16 @@ E2_D void note_finished(Ctx& x, i64 id, double now, i64 out) {
 // Clear [start, end) of the root path ending at `bottom`, deepest first
 // (the second half of uncache_suffix, prefix_tree.cpp:262-270).  The node
 // containing `start` has already been split there.
-E2_D i64 clear_range_from(Ctx& x, u32 bottom, i64 start, int g) {
+E2_DNI i64 clear_range_from(u32 bottom, i64 start, int g) {
   i64 freed = 0;
   for (u32 v = bottom; v != kRoot && v != kNil;) {
-    const NodeRec* r = nget(x, v);
+    const NodeRec* r = nget(v);
     const i64 v_end = (i64)r->depth + r->edge_len;
     if (v_end <= start) break;
     const u32 p = r->parent;
     if (rcached(r, g)) {
       freed += r->edge_len;
-      clear_cached(x, v, g);
+      clear_cached(v, g);
     }
     v = p;
   }
@@ -734,9 +719,7 @@ E2_D i64 clear_range_from(Ctx& x, u32 bottom, i64 start, int g) {
 
 // uncache_suffix (prefix_tree.cpp:237-271) for a sequence whose matched
 // length M is known.  Warp-wide.  Returns tokens uncached.
-E2_D i64 uncache_suffix(Ctx& x, const i32* seq, i64 n, i64 M, i64 tail_len, int g) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
+E2_DNI i64 uncache_suffix(const i32* seq, i64 n, i64 M, i64 tail_len, int g) {
   if (n == 0 || tail_len <= 0) return 0;
   const i64 end = min_(n, M);
   i64 start = n - tail_len;
@@ -746,82 +729,80 @@ E2_D i64 uncache_suffix(Ctx& x, const i32* seq, i64 n, i64 M, i64 tail_len, int 
   i64 off = 0;
   u32 cur = kRoot, bottom = kNil;
   while (off < end) {
-    const u32 ch = child_lookup(d, cur, seq[off]);
+    const u32 ch = child_lookup(cur, seq[off]);
     if (ch == kNil) {
-      if (lane0()) set_err(h, kErrSim, kWhyWalk);
+      if (lane0()) set_err(kErrSim, kWhyWalk);
       wsync();
       return 0;
     }
-    const i64 len = nget(x, ch)->edge_len;
+    const i64 len = nget(ch)->edge_len;
     const i64 m = min_(len, M - off);
     u32 node = ch;
     if (m < len) {
-      node = split_node(x, ch, (u32)m);  // keep the part on seq's path
+      node = split_node(ch, (u32)m);  // keep the part on seq's path
       if (node == kNil) return 0;
     }
     const i64 node_end = off + m;
     if (node_end > start && off < start) {
       // split at start: the slot keeps the suffix, which is the target
-      if (split_node(x, node, (u32)(start - off)) == kNil) return 0;
+      if (split_node(node, (u32)(start - off)) == kNil) return 0;
     }
     bottom = node;
     cur = node;
     off = node_end;
     if (m < len) break;
   }
-  return clear_range_from(x, bottom, start, g);
+  return clear_range_from(bottom, start, g);
 }
 
 // uncache_suffix for a prompt committed earlier in this replay: its tail
 // slot (the node ending at |p|) is stable under splits, so the path is the
 // parent chain and no token is read.  Warp-wide.
-E2_D i64 uncache_tail(Ctx& x, u32 tail, i64 n, i64 tail_len, int g) {
+E2_DNI i64 uncache_tail(u32 tail, i64 n, i64 tail_len, int g) {
   if (n == 0 || tail_len <= 0 || tail == kNil) return 0;
   i64 start = n - tail_len;
   if (start < 0) start = 0;
   if (start >= n) return 0;
   // find the node containing `start` on the chain and split there
   for (u32 v = tail; v != kRoot;) {
-    const NodeRec* r = nget(x, v);
+    const NodeRec* r = nget(v);
     const i64 dep = r->depth;
     const u32 p = r->parent;
     if (dep <= start) {
-      if (dep < start && split_node(x, v, (u32)(start - dep)) == kNil) return 0;
+      if (dep < start && split_node(v, (u32)(start - dep)) == kNil) return 0;
       break;
     }
     v = p;
   }
-  return clear_range_from(x, tail, start, g);
+  return clear_range_from(tail, start, g);
 }
 
 // Mirror-LRU eviction: plan_eviction(g, over, {}, partial)
 // then note_eviction for every entry, ranges built before any is applied.
-E2_D void evict_lru(Ctx& x, int g, i64 over) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
+E2_DNI void evict_lru(int g, i64 over) {
   if (lane0()) {
     u32 nv = 0;
-    plan_eviction(x, g, over, true, [&](u32 v, i64 tok, const NodeRec*) {
-      if (nv < d.vcap) {
-        d.vic_slot[nv] = v;
-        d.vic_tok[nv] = tok;
+    plan_eviction(g, over, true, [&](u32 v, i64 tok, const NodeRec*) {
+      if (nv < DEV.vcap) {
+        DEV.vic_slot[nv] = v;
+        DEV.vic_tok[nv] = tok;
         nv++;
       } else {
-        set_err(h, kErrCapacity, kWhyScratchCap);
+        set_err(kErrCapacity, kWhyScratchCap);
       }
     });
-    d.scr_val[(u64)d.cfg.G * d.scap] = nv;  // count, in the spare scratch word
+    DEV.scr_val[(u64)DEV.cfg.G * DEV.scap] = nv;  // count, in the spare scratch word
   }
   wsync();
-  const u32 nv = (u32)d.scr_val[(u64)d.cfg.G * d.scap];
-  for (u32 i = 0; i < nv && !h->err; ++i) {
-    const u32 v = d.vic_slot[i];
-    const i64 tok = d.vic_tok[i];
-    const i64 len = nget(x, v)->edge_len;
+  const u32 nv = (u32)DEV.scr_val[(u64)DEV.cfg.G * DEV.scap];
+  for (u32 i = 0; i < nv && !HOT.err; ++i) {
+    const u32 v = DEV.vic_slot[i];
+    const i64 tok = DEV.vic_tok[i];
+    const i64 len = nget(v)->edge_len;
     if (tok < len) {
-      if (split_node(x, v, (u32)(len - tok)) == kNil) return;
+      if (split_node(v, (u32)(len - tok)) == kNil) return;
     }
-    clear_cached(x, v, g);
+    clear_cached(v, g);
   }
 }
 

@@ -70,17 +70,17 @@ struct SerialArgs {
 
 // Bring every instance's window and hit counters current at `now`
 // (export / dump / dead-node removal read hits for all instances).  Warp-wide.
-E2_D void expire_all(Ctx& x, double now) {
-  const int G = x.d.cfg.G;
-  for (int g = lane(); g < G; g += kWidth) win_prune(x.d, x.h, g, now);
+E2_D void expire_all(double now) {
+  const int G = DEV.cfg.G;
+  for (int g = lane(); g < G; g += kWidth) win_prune(g, now);
   wsync();
-  for (int g = 0; g < G; ++g) hits_catchup(x, g);
+  for (int g = 0; g < G; ++g) hits_catchup(g);
 }
 
-E2_D void write_decision(const Dev& d, const Scr* s, const Dec& r, i64 req_id, e2_decision* dec,
+E2_D void write_decision(const Scr* s, const Dec& r, i64 req_id, e2_decision* dec,
                          e2_cost* costs, double* ratios) {
-  const int G = d.cfg.G;
-  const bool cost_path = (r.branch == 0 || r.branch == 1) && d.cfg.mode == 0;
+  const int G = DEV.cfg.G;
+  const bool cost_path = (r.branch == 0 || r.branch == 1) && DEV.cfg.mode == 0;
   const int nc = cost_path ? s->n_costs : 0;
   if (lane0()) {
     dec->request = req_id;
@@ -115,20 +115,18 @@ E2_D void write_decision(const Dev& d, const Scr* s, const Dec& r, i64 req_id, e
 // Dead-node removal (prefix_tree.cpp:357-378): a node goes when it is
 // uncached, childless and has no in-window hit on any instance; repeat until
 // a fixpoint (the reference removes bottom-up in one DFS).  Warp-wide.
-E2_D i64 prune_dead(Ctx& x) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
-  const int G = d.cfg.G;
+E2_D i64 prune_dead() {
+  const int G = DEV.cfg.G;
   i64 removed = 0;
   bool again = true;
   while (again) {
     again = false;
-    const u32 used = h->slots_used;
+    const u32 used = HOT.slots_used;
     for (u32 b = 1; b < used; b += 32) {
       u32 m = vote(32, [&](int j) {
         const u32 sl = b + (u32)j;
         if (sl >= used) return false;
-        const NodeRec* r = npeek(x, sl);
+        const NodeRec* r = npeek(sl);
         if (r->edge_len == 0 || r->cmask != 0 || r->nchild != 0) return false;
         for (int g = 0; g < G; ++g)
           if (rhits(r, G)[g] != 0) return false;
@@ -139,22 +137,22 @@ E2_D i64 prune_dead(Ctx& x) {
         const int j = ffs32(m);
         m &= m - 1;
         const u32 v = b + (u32)j;
-        NodeRec* rv = nget(x, v);
+        NodeRec* rv = nget(v);
         const u32 par = rv->parent;
         const i32 ft = rv->first_tok;
         wsync();
         if (lane0()) {
           rv->edge_len = 0;
           rv->parent = kNil;
-          ndirty(x, rv);
-          h->node_count--;
+          ndirty(rv);
+          HOT.node_count--;
         }
         wsync();
-        child_erase(d, h, par, ft);
-        NodeRec* rp = nget(x, par);
+        child_erase(par, ft);
+        NodeRec* rp = nget(par);
         if (lane0()) {
           rp->nchild -= 1;
-          ndirty(x, rp);
+          ndirty(rp);
         }
         wsync();
         removed++;
@@ -167,30 +165,28 @@ E2_D i64 prune_dead(Ctx& x) {
 
 // Subtree walks for autoscale replication (global_scheduler.cpp:299-338):
 // children are found by scanning parents (rare path).
-E2_D void subtree_apply(Ctx& x, u32 root, int g, double now, bool mark) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
+E2_D void subtree_apply(u32 root, int g, double now, bool mark) {
   u32 top = 0;
-  if (lane0()) d.vic_slot[0] = root;
+  if (lane0()) DEV.vic_slot[0] = root;
   wsync();
   top = 1;
   u32 order = 0;
   // collect the subtree (breadth-first) into vic_slot, then apply
   while (order < top) {
-    const u32 p = d.vic_slot[order++];
-    const u32 used = h->slots_used;
+    const u32 p = DEV.vic_slot[order++];
+    const u32 used = HOT.slots_used;
     for (u32 b = 1; b < used; b += 32) {
       const u32 m = vote(32, [&](int j) {
         const u32 sl = b + (u32)j;
         if (sl >= used) return false;
-        const NodeRec* r = npeek(x, sl);
+        const NodeRec* r = npeek(sl);
         return r->edge_len > 0 && r->parent == p;
       });
       wsync();
       if (lane0()) {
         u32 mm = m, t = top;
         while (mm) {
-          d.vic_slot[t++] = b + (u32)ffs32(mm);
+          DEV.vic_slot[t++] = b + (u32)ffs32(mm);
           mm &= mm - 1;
         }
       }
@@ -200,67 +196,65 @@ E2_D void subtree_apply(Ctx& x, u32 root, int g, double now, bool mark) {
   }
   if (mark) {
     for (u32 i = 0; i < top; ++i) {
-      const u32 v = d.vic_slot[i];
+      const u32 v = DEV.vic_slot[i];
       if (v == kRoot) continue;
-      set_cached(x, v, g);
-      touch_la(x, v, g, now);
+      set_cached(v, g);
+      touch_la(v, g, now);
     }
   } else {
     for (u32 i = top; i-- > 0;) {  // children before parents
-      const u32 v = d.vic_slot[i];
-      if (v != kRoot) clear_cached(x, v, g);
+      const u32 v = DEV.vic_slot[i];
+      if (v != kRoot) clear_cached(v, g);
     }
   }
 }
 
-E2_D void api_op(Ctx& x, Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
-  const int G = d.cfg.G;
-  const i32* seq = d.tok + op.off;
+E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
+  const int G = DEV.cfg.G;
+  const i32* seq = DEV.tok + op.off;
   switch (op.kind) {
     case OP_SCHEDULE:
     case OP_DECIDE: {
       const bool commit_it = op.kind == OP_SCHEDULE;
-      if (commit_it && d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(x, s, op.now);
+      if (commit_it && DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, op.now);
       Walk w;
-      Dec r = decide(x, s, seq, op.len, op.L, hint, kPathHint, op.now, w);
+      Dec r = decide(s, seq, op.len, op.L, hint, kPathHint, op.now, w);
       if (!r.ok) return;
       if (commit_it) {
-        commit(x, op.off, op.len, op.L, w, r, op.id, op.arr, op.now);
-        if (h->err) return;
-        count_stats(h, r);
+        commit(op.off, op.len, op.L, w, r, op.id, op.arr, op.now);
+        if (HOT.err) return;
+        count_stats(r);
       }
-      write_decision(d, s, r, op.id, &out->dec, out->costs, out->ratios);
+      write_decision(s, r, op.id, &out->dec, out->costs, out->ratios);
       break;
     }
     case OP_PREFILL: {
-      if (d.cfg.mode != 0 || op.len == 0) break;
-      Walk w = walk_known(x, seq, op.L, hint, kPathHint, s->ext);
+      if (DEV.cfg.mode != 0 || op.len == 0) break;
+      Walk w = walk_known(seq, op.L, hint, kPathHint, s->ext);
       if (!w.ok) {
-        if (lane0()) set_err(h, kErrSim, kWhyWalk);
+        if (lane0()) set_err(kErrSim, kWhyWalk);
         wsync();
         return;
       }
-      u32 tail = ensure_path(x, op.off, op.len, op.L, w);
-      if (tail == kNil || h->err) return;
-      mark_cached_chain(x, tail, op.gpu, op.now);
+      u32 tail = ensure_path(op.off, op.len, op.L, w);
+      if (tail == kNil || HOT.err) return;
+      mark_cached_chain(tail, op.gpu, op.now);
       break;
     }
     case OP_EVICT: {
-      if (d.cfg.mode != 0) break;
-      i64 f = uncache_suffix(x, seq, op.len, op.L, op.x, op.gpu);
+      if (DEV.cfg.mode != 0) break;
+      i64 f = uncache_suffix(seq, op.len, op.L, op.x, op.gpu);
       if (lane0()) out->i0 = f;
       wsync();
       break;
     }
     case OP_FINISHED:
-      note_finished(x, op.id, op.now, op.x);
+      note_finished(op.id, op.now, op.x);
       break;
     case OP_LOAD_COST: {
-      cost_prepare(x, op.gpu, op.x, op.now);
+      cost_prepare(op.gpu, op.x, op.now);
       if (lane0()) {
-        CostOut c = cost_for(x, op.gpu, op.x, op.now);
+        CostOut c = cost_for(op.gpu, op.x, op.now);
         out->costs[0].gpu = op.gpu;
         out->costs[0].eviction_infeasible = c.inf ? 1 : 0;
         out->costs[0].current_load_ms = c.L;
@@ -271,12 +265,12 @@ E2_D void api_op(Ctx& x, Scr* s, const OpDesc& op, const u32* hint, ApiOut* out)
       break;
     }
     case OP_GPU_LOAD: {
-      if (lane0()) out->v = win_load(d, h, op.gpu, op.now);
+      if (lane0()) out->v = win_load(op.gpu, op.now);
       wsync();
       break;
     }
     case OP_MATCH: {
-      Walk w = walk_known(x, seq, op.L, hint, kPathHint, s->ext);
+      Walk w = walk_known(seq, op.L, hint, kPathHint, s->ext);
       for (int g = lane(); g < G; g += kWidth) out->ext[g] = ((w.present >> g) & 1ull) ? s->ext[g] : 0;
       if (lane0()) {
         out->i0 = op.L;
@@ -286,15 +280,15 @@ E2_D void api_op(Ctx& x, Scr* s, const OpDesc& op, const u32* hint, ApiOut* out)
       break;
     }
     case OP_EXPIRE_ALL:
-      expire_all(x, op.now);
+      expire_all(op.now);
       break;
     case OP_WINDOW: {
       if (lane0()) {
-        win_prune(d, h, op.gpu, op.now);
-        out->i0 = (i64)(h->ws_tail[op.gpu] - h->ws_head[op.gpu]);
-        out->i1 = (i64)(h->wc_tail[op.gpu] - h->wc_head[op.gpu]);
-        out->i2 = h->inflight_cached[op.gpu];
-        out->i3 = h->inflight_prompt[op.gpu];
+        win_prune(op.gpu, op.now);
+        out->i0 = (i64)(HOT.ws_tail[op.gpu] - HOT.ws_head[op.gpu]);
+        out->i1 = (i64)(HOT.wc_tail[op.gpu] - HOT.wc_head[op.gpu]);
+        out->i2 = HOT.inflight_cached[op.gpu];
+        out->i3 = HOT.inflight_prompt[op.gpu];
       }
       wsync();
       break;
@@ -302,20 +296,20 @@ E2_D void api_op(Ctx& x, Scr* s, const OpDesc& op, const u32* hint, ApiOut* out)
     case OP_INFLIGHT_GET: {
       if (lane0()) {
         bool found;
-        u64 i = inf_find(d, op.id, found);
+        u64 i = inf_find(op.id, found);
         out->i0 = found ? 1 : 0;
         if (found) {
-          out->u0 = d.inf[i].root;
-          out->v = d.inf[i].arr;
-          out->i1 = d.inf[i].gpu;
+          out->u0 = DEV.inf[i].root;
+          out->v = DEV.inf[i].arr;
+          out->i1 = DEV.inf[i].gpu;
         }
       }
       wsync();
       break;
     }
     case OP_PRUNE_DEAD: {
-      expire_all(x, op.now);
-      i64 rm = prune_dead(x);
+      expire_all(op.now);
+      i64 rm = prune_dead();
       if (lane0()) out->i0 = rm;
       wsync();
       break;
@@ -323,16 +317,16 @@ E2_D void api_op(Ctx& x, Scr* s, const OpDesc& op, const u32* hint, ApiOut* out)
     case OP_MARK_NODE: {
       u32 v = (u32)op.x;
       if (v != kRoot) {
-        set_cached(x, v, op.gpu);
-        touch_la(x, v, op.gpu, op.now);
+        set_cached(v, op.gpu);
+        touch_la(v, op.gpu, op.now);
       }
       break;
     }
     case OP_MARK_SUBTREE:
-      subtree_apply(x, (u32)op.x, op.gpu, op.now, true);
+      subtree_apply((u32)op.x, op.gpu, op.now, true);
       break;
     case OP_UNCACHE_SUBTREE:
-      subtree_apply(x, (u32)op.x, op.gpu, op.now, false);
+      subtree_apply((u32)op.x, op.gpu, op.now, false);
       break;
     default:
       break;
@@ -340,80 +334,77 @@ E2_D void api_op(Ctx& x, Scr* s, const OpDesc& op, const u32* hint, ApiOut* out)
 }
 
 // One request of the generalised criterion-7 loop (e2sched.h, e2_replay).
-E2_D void replay_step(Ctx& x, Scr* s, const SerialArgs& a, i64 li) {
-  const Dev& d = x.d;
-  Hot* h = x.h;
-  const int G = d.cfg.G;
+E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
+  const int G = DEV.cfg.G;
   const i64 r = a.base + li;
   const i64 off = a.off[r], n = a.len[r];
-  const i32* seq = d.tok + off;
-  const double now = max_(h->drv_now, a.arr[r]);
-  if (lane0()) h->drv_now = now;
+  const i32* seq = DEV.tok + off;
+  const double now = max_(HOT.drv_now, a.arr[r]);
+  if (lane0()) HOT.drv_now = now;
   wsync();
-  if (d.cfg.mode == 0 && d.cfg.rebalance && G > 1) update_redirects(x, s, now);
+  if (DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, now);
   Walk w;
-  Dec dec = decide(x, s, seq, n, a.L[li], a.hint + li * kPathHint, kPathHint, now, w);
+  Dec dec = decide(s, seq, n, a.L[li], a.hint + li * kPathHint, kPathHint, now, w);
   if (!dec.ok) return;
-  const u32 tail = commit(x, off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now);
-  if (h->err) return;
-  if (lane0()) d.req_tail[r] = tail;
-  count_stats(h, dec);
-  write_decision(d, s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
+  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now);
+  if (HOT.err) return;
+  if (lane0()) DEV.req_tail[r] = tail;
+  count_stats(dec);
+  write_decision(s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
                  a.ratios ? a.ratios + r * G : nullptr);
   const int g = dec.gpu;
-  if (a.prefill && d.cfg.mode == 0) mark_cached_chain(x, tail, g, now);
-  if (h->err) return;
+  if (a.prefill && DEV.cfg.mode == 0) mark_cached_chain(tail, g, now);
+  if (HOT.err) return;
   if (a.eviction == E2_EVICT_FIFO_TAIL) {
     if (lane0()) {
-      u64 t = h->fifo_tail[g];
-      u64 i = (u64)g * d.fcap + (t & (d.fcap - 1));
-      if (t - h->fifo_head[g] >= d.fcap) set_err(h, kErrCapacity, kWhyFifoCap);
-      d.fifo_req[i] = r;
-      d.fifo_tail[i] = n - a.trunk;
-      h->fifo_tail[g] = t + 1;
+      u64 t = HOT.fifo_tail[g];
+      u64 i = (u64)g * DEV.fcap + (t & (DEV.fcap - 1));
+      if (t - HOT.fifo_head[g] >= DEV.fcap) set_err(kErrCapacity, kWhyFifoCap);
+      DEV.fifo_req[i] = r;
+      DEV.fifo_tail[i] = n - a.trunk;
+      HOT.fifo_tail[g] = t + 1;
     }
     wsync();
-    while (h->cached_tokens[g] > a.hw && h->fifo_head[g] < h->fifo_tail[g] && !h->err) {
-      u64 i = (u64)g * d.fcap + (h->fifo_head[g] & (d.fcap - 1));
-      const i64 k = d.fifo_req[i], tl = d.fifo_tail[i];
+    while (HOT.cached_tokens[g] > a.hw && HOT.fifo_head[g] < HOT.fifo_tail[g] && !HOT.err) {
+      u64 i = (u64)g * DEV.fcap + (HOT.fifo_head[g] & (DEV.fcap - 1));
+      const i64 k = DEV.fifo_req[i], tl = DEV.fifo_tail[i];
       wsync();
-      if (lane0()) h->fifo_head[g]++;
+      if (lane0()) HOT.fifo_head[g]++;
       wsync();
-      if (d.cfg.mode == 0) uncache_tail(x, d.req_tail[k], a.len[k], tl, g);
+      if (DEV.cfg.mode == 0) uncache_tail(DEV.req_tail[k], a.len[k], tl, g);
     }
   } else if (a.eviction == E2_EVICT_MIRROR_LRU) {
-    const i64 cached = h->cached_tokens[g];
-    if (cached > a.hw && d.cfg.mode == 0) evict_lru(x, g, cached - a.hw);
+    const i64 cached = HOT.cached_tokens[g];
+    if (cached > a.hw && DEV.cfg.mode == 0) evict_lru(g, cached - a.hw);
   }
-  if (h->err) return;
+  if (HOT.err) return;
   if (li + a.base >= a.lag) {
     const i64 k = r - a.lag;
-    note_finished(x, a.ids[k], now, a.outl[k]);
+    note_finished(a.ids[k], now, a.outl[k]);
   }
 }
 
-E2_D void serial_body(Ctx& x, Scr* s, const SerialArgs& a) {
-  Hot* h = x.h;
-  if (lane0()) h->done = 0;
+E2_D void serial_body(Scr* s, const SerialArgs& a) {
+  if (lane0()) HOT.done = 0;
   wsync();
   if (a.kind == 0) {
     i64 i = 0;
     for (; i < a.n; ++i) {
-      replay_step(x, s, a, i);
-      if (h->err) {
-        if (lane0()) h->err_req = a.base + i;
+      replay_step(s, a, i);
+      if (HOT.err) {
+        if (lane0()) HOT.err_req = a.base + i;
         wsync();
         break;
       }
     }
-    if (lane0()) h->done = i;
+    if (lane0()) HOT.done = i;
     wsync();
   } else {
-    api_op(x, s, a.op, a.hint, a.out);
-    if (lane0()) h->done = h->err ? 0 : 1;
+    api_op(s, a.op, a.hint, a.out);
+    if (lane0()) HOT.done = HOT.err ? 0 : 1;
     wsync();
   }
-  nflush(x);
+  nflush();
 }
 
 }  // namespace e2

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -123,24 +124,22 @@ namespace {
 constexpr int kMatchWarpsPerBlock = 8;
 
 #if E2_DEVICE_BUILD
-__global__ void __launch_bounds__(32, 1) k_serial(Dev d, SerialArgs a, u32 nsets) {
-  __shared__ Hot hs;
+__global__ void __launch_bounds__(32, 1) k_serial(SerialArgs a, u32 nsets) {
   __shared__ Scr ss;
-  __shared__ NCache nc;
   extern __shared__ __align__(16) char dyn[];
   const u32 ne = nsets * kWays;
   {
-    const u64* src = (const u64*)d.hot_g;
-    u64* dst = (u64*)&hs;
+    const u64* src = (const u64*)g_dev.hot_g;
+    u64* dst = (u64*)&g_hot;
     for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
   }
   if (threadIdx.x == 0) {
-    nc.nsets = nsets;
-    nc.clock = 0;
-    nc.tag = (u32*)dyn;
-    nc.tick = nc.tag + ne;
-    nc.dirty = nc.tick + ne;
-    nc.data = dyn + ((3 * ne * 4 + 15) / 16) * 16;
+    g_nc.nsets = nsets;
+    g_nc.clock = 0;
+    g_nc.tag = (u32*)dyn;
+    g_nc.tick = g_nc.tag + ne;
+    g_nc.dirty = g_nc.tick + ne;
+    g_nc.data = dyn + ((3 * ne * 4 + 15) / 16) * 16;
   }
   for (u32 i = threadIdx.x; i < ne; i += 32) {
     ((u32*)dyn)[i] = kNil;
@@ -148,26 +147,22 @@ __global__ void __launch_bounds__(32, 1) k_serial(Dev d, SerialArgs a, u32 nsets
     ((u32*)dyn)[2 * ne + i] = 0;
   }
   __syncwarp();
-  Ctx x;
-  x.d = d;
-  x.h = &hs;
-  x.c = &nc;
-  serial_body(x, &ss, a);
+  serial_body(&ss, a);
   __syncwarp();
   {
-    const u64* src = (const u64*)&hs;
-    u64* dst = (u64*)d.hot_g;
+    const u64* src = (const u64*)&g_hot;
+    u64* dst = (u64*)g_dev.hot_g;
     for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
   }
 }
 
-__global__ void __launch_bounds__(kMatchWarpsPerBlock * 32) k_match(Dev d, i64 n, i64 base, const i64* off,
+__global__ void __launch_bounds__(kMatchWarpsPerBlock * 32) k_match(i64 n, i64 base, const i64* off,
                                                                      const i64* len, i64* S, u32* dslot, u32* dm,
                                                                      u32* path, unsigned long long* bytes) {
   const i64 w = (i64)blockIdx.x * kMatchWarpsPerBlock + (threadIdx.x >> 5);
   if (w >= n) return;
   const i64 r = base + w;
-  MatchRes m = match_one(d, d.tok + off[r], len[r], path + w * kPathHint);
+  MatchRes m = match_one(g_dev.tok + off[r], len[r], path + w * kPathHint);
   if (lane0()) {
     S[w] = m.S;
     dslot[w] = m.div_slot;
@@ -198,7 +193,7 @@ __device__ __forceinline__ u32 gtab_find(const u64* tk, const u32* tv, u64 mask,
   }
 }
 
-__global__ void k_group_init(Dev d, i64 n, i64 base, const i64* off, const i64* len, const i64* S, const u32* dslot,
+__global__ void k_group_init(i64 n, i64 base, const i64* off, const i64* len, const i64* S, const u32* dslot,
                              const u32* dm, i32* state, u64* A, u64* B, i64* cand, i64* L, u64* tk, u32* tv,
                              u64 mask) {
   i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -212,7 +207,7 @@ __global__ void k_group_init(Dev d, i64 n, i64 base, const i64* off, const i64* 
   }
   state[i] = 1;
   A[i] = ((u64)dslot[i] << 32) | (u64)dm[i];
-  B[i] = (u64)(u32)d.tok[off[r] + s];
+  B[i] = (u64)(u32)g_dev.tok[off[r] + s];
   cand[i] = s;
   gtab_insert(tk, tv, mask, gkey(A[i], B[i], 0), (u32)i);
 }
@@ -240,7 +235,7 @@ __global__ void k_group_resolve(i64 n, int round, i32* state, const u64* A, cons
 }
 
 __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32)
-    k_group_round(Dev d, i64 n, i64 base, int round, const i64* off, const i64* len, i32* state, u64* A, u64* B,
+    k_group_round(i64 n, i64 base, int round, const i64* off, const i64* len, i32* state, u64* A, u64* B,
                   i64* cand, const i64* leader, const i64* o, i64* L, u64* tk, u32* tv, u64 mask,
                   unsigned long long* bytes) {
   const i64 i = (i64)blockIdx.x * kMatchWarpsPerBlock + (threadIdx.x >> 5);
@@ -248,7 +243,7 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32)
   const i64 r = base + i, l = leader[i], rl = base + l;
   const i64 oi = o[i], ni = len[r], nl = len[rl];
   const i64 lim = min_(ni, nl) - oi;
-  const i64 a = oi + warp_lcp(d.tok + off[r] + oi, d.tok + off[rl] + oi, lim);
+  const i64 a = oi + warp_lcp(g_dev.tok + off[r] + oi, g_dev.tok + off[rl] + oi, lim);
   if (lane0()) {
     atomicAdd(bytes, (unsigned long long)(8 * (a - oi + 1)));
     if (a >= ni) {
@@ -256,7 +251,7 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32)
       L[i] = a;
     } else {
       A[i] = ((u64)l << 32) | (u64)a;
-      B[i] = (u64)(u32)d.tok[off[r] + a];
+      B[i] = (u64)(u32)g_dev.tok[off[r] + a];
       cand[i] = a;
       gtab_insert(tk, tv, mask, gkey(A[i], B[i], round), (u32)i);
     }
@@ -382,6 +377,15 @@ struct Timed {
 };
 void prof_flush(e2_handle*) {}
 #endif
+
+// The kernels read the handle's pointers/config from constant memory.
+void upload_dev(e2_handle* h) {
+#if E2_DEVICE_BUILD
+  CK(cudaMemcpyToSymbolAsync(g_dev, &h->d, sizeof(Dev), 0, cudaMemcpyHostToDevice, h->stream));
+#else
+  g_dev_h = h->d;
+#endif
+}
 
 void push_hot(e2_handle* h) { h2d(h->d.hot_g, &h->hot, sizeof(Hot), h->stream); }
 void pull_hot(e2_handle* h) {
@@ -646,7 +650,8 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
     Timed t(h, a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER);
 #if E2_DEVICE_BUILD
     h->acc.launches[a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER]++;
-    k_serial<<<1, 32, h->serial_smem, h->stream>>>(h->d, a, h->nsets);
+    upload_dev(h);
+    k_serial<<<1, 32, h->serial_smem, h->stream>>>(a, h->nsets);
     CK(cudaGetLastError());
 #else
     Scr s;
@@ -662,11 +667,10 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
     nc.tick = tick.data();
     nc.dirty = dirty.data();
     nc.data = (char*)data.data();
-    Ctx x;
-    x.d = h->d;
-    x.h = h->d.hot_g;
-    x.c = &nc;
-    serial_body(x, &s, a);
+    g_dev_h = h->d;
+    g_hot_h = h->d.hot_g;
+    g_nc_h = nc;
+    serial_body(&s, a);
 #endif
   }
 }
@@ -682,7 +686,8 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
     Timed t(h, E2_K_MATCH);
     unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
     h->acc.launches[E2_K_MATCH]++;
-    k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(d, n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
+    upload_dev(h);
+    k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
                                                              h->b_dm, h->b_path, h->d_bytes);
     CK(cudaGetLastError());
   }
@@ -698,7 +703,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   dset(h->g_tk, 0, tsz * 8, h->stream);
   dset(h->g_tv, 0xff, tsz * 4, h->stream);
   h->acc.launches[E2_K_GROUP]++;
-  k_group_init<<<tg, 256, 0, h->stream>>>(d, n, base, h->r_off, h->r_len, h->b_S, h->b_dslot, h->b_dm, h->b_state,
+  k_group_init<<<tg, 256, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot, h->b_dm, h->b_state,
                                           h->b_A, h->b_B, h->b_cand, h->b_L, h->g_tk, h->g_tv, h->g_mask);
   CK(cudaGetLastError());
   for (int round = 0;; ++round) {
@@ -717,7 +722,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
     unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
     h->acc.launches[E2_K_GROUP]++;
     k_group_round<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(
-        d, n, base, round + 1, h->r_off, h->r_len, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
+        n, base, round + 1, h->r_off, h->r_len, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
         h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_bytes + 1);
     CK(cudaGetLastError());
   }
@@ -727,7 +732,8 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   std::vector<u32> ds(n), dm(n);
   for (i64 w = 0; w < n; ++w) {
     const i64 r = base + w;
-    MatchRes m = match_one(d, d.tok + h->r_off[r], h->r_len[r], h->b_path + w * kPathHint);
+    g_dev_h = h->d;
+    MatchRes m = match_one(d.tok + h->r_off[r], h->r_len[r], h->b_path + w * kPathHint);
     S[w] = m.S;
     ds[w] = m.div_slot;
     dm[w] = m.div_m;
@@ -827,8 +833,11 @@ void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match) 
   check_hot_error(h);
 }
 
+std::recursive_mutex g_lock;  // g_dev (constant memory) is shared by every handle
+
 template <typename F>
 int guard(e2_handle* h, F&& f) {
+  std::lock_guard<std::recursive_mutex> lk(g_lock);
   try {
     f();
     return E2_OK;

@@ -58,7 +58,7 @@ struct MatchRes {
 };
 
 // Warp-wide walk with token comparison; records up to kPathHint path slots.
-E2_D MatchRes match_one(const Dev& d, const i32* seq, i64 n, u32* path) {
+E2_D MatchRes match_one(const i32* seq, i64 n, u32* path) {
   MatchRes r;
   r.S = 0;
   r.div_slot = kRoot;
@@ -67,14 +67,14 @@ E2_D MatchRes match_one(const Dev& d, const i32* seq, i64 n, u32* path) {
   u32 cur = kRoot;
   int level = 0;
   while (pos < n) {
-    const u32 ch = child_lookup(d, cur, seq[pos]);
+    const u32 ch = child_lookup(cur, seq[pos]);
     depth++;
     if (ch == kNil) break;
-    const NodeRec* hd = grec(d, ch);
+    const NodeRec* hd = grec(ch);
     const i64 off = hd->edge_off, len = hd->edge_len;
     const i64 lim = min_(len, n - pos);
     // first token equal by construction of the child key
-    const i64 m = 1 + warp_lcp(d.tok + off + 1, seq + pos + 1, lim - 1);
+    const i64 m = 1 + warp_lcp(DEV.tok + off + 1, seq + pos + 1, lim - 1);
     if (path && level < kPathHint && lane0()) path[level] = ch;
     level++;
     pos += m;
