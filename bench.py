@@ -29,7 +29,7 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-from paper_2407_00023_b200 import abi, workload  # noqa: E402
+from paper_2407_00023_b200 import abi, replicas, workload  # noqa: E402
 from paper_2407_00023_b200.scheduler import COST_DTYPE, DECISION_DTYPE, GlobalScheduler  # noqa: E402
 
 METRIC = "scheduling decisions/sec (E2 placement replay)"
@@ -106,11 +106,7 @@ class ClockSampler:
         }
 
 
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+dist_env = replicas.dist_env
 
 
 def cpu_reference_replay(cfg, trace, repeats_s: float = 10.0, max_runs: int = 3):
@@ -288,19 +284,14 @@ def run_b200(args):
     assert np.array_equal(dec, dec_e2e), "device-resident and host-buffer replays disagree"
 
     # max over ranks
-    if ws > 1:
-        t = torch.tensor([ms, statistics.mean(e2e_ms)], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, e2e_max = float(t[0]), float(t[1])
-    else:
-        e2e_max = statistics.mean(e2e_ms)
+    ms, e2e_max = replicas.max_over_ranks([ms, statistics.mean(e2e_ms)], device=dev)
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
         return 0
 
-    value = ws * n / (ms / 1000.0)
-    e2e_value = ws * n / (e2e_max / 1000.0)
+    value = replicas.job_throughput(ws, n, ms)
+    e2e_value = replicas.job_throughput(ws, n, e2e_max)
     peak, peak_kind = _peaks()
     steps = args.steps
     match_ms = prof.ms[abi.E2_K_MATCH] / max(1, prof.launches[abi.E2_K_MATCH])
@@ -311,7 +302,9 @@ def run_b200(args):
     if os.path.exists(tp):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                per_req = json.load(f).get("dram_bytes_per_request")
+            # same per-launch normalisation as `achieved`
+            traffic = per_req * prof.match_requests / max(1, prof.launches[abi.E2_K_MATCH])
         except Exception:
             traffic = None
     total_kernel_ms = sum(prof.ms)

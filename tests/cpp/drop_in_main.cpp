@@ -1,0 +1,90 @@
+// The reference's own criterion-7 loop (acceptance_main.cpp:367-416), run
+// twice in lock step: once on kvsched::GlobalScheduler (the unmodified
+// reference, compiled from its sources) and once on the drop-in
+// kvsched::b200::GlobalScheduler (include/e2sched.hpp over the C ABI).
+// Every Decision field and cost double must match.  Exit 0 on success.
+#include <cstdio>
+#include <cstdlib>
+#include <deque>
+
+#include "e2sched.hpp"
+#include "kvsched/workload.hpp"
+
+using namespace kvsched;
+
+static bool same(const Decision& a, const Decision& b) {
+  if (a.branch != b.branch || a.gpu != b.gpu || a.redirected != b.redirected ||
+      a.pre_redirect_gpu != b.pre_redirect_gpu || a.cached_len != b.cached_len || a.missed_len != b.missed_len ||
+      a.missed_on_chosen != b.missed_on_chosen || a.costs.size() != b.costs.size() ||
+      a.decode_ratios != b.decode_ratios)
+    return false;
+  for (size_t i = 0; i < a.costs.size(); ++i) {
+    const CostBreakdown &x = a.costs[i].cost, &y = b.costs[i].cost;
+    if (a.costs[i].gpu != b.costs[i].gpu || x.current_load_ms != y.current_load_ms ||
+        x.eviction_ms != y.eviction_ms || x.prefill_ms != y.prefill_ms ||
+        x.eviction_infeasible != y.eviction_infeasible)
+      return false;
+  }
+  return true;
+}
+
+template <typename S>
+static void step(S& s, std::vector<std::deque<std::pair<const TokenSeq*, int64_t>>>& cached, const Request& r,
+                 SimTime now, int64_t trunk, const Decision& d) {
+  s.note_prefill_cached(r.prompt, d.gpu, now);
+  cached[d.gpu].push_back({&r.prompt, static_cast<int64_t>(r.prompt.size()) - trunk});
+  auto cached_tokens = [&](GpuId g) {
+    if constexpr (std::is_same_v<S, kvsched::GlobalScheduler>)
+      return s.mirror().cached_tokens(g);
+    else
+      return s.cached_tokens(g);
+  };
+  while (cached_tokens(d.gpu) > 150000 && !cached[d.gpu].empty()) {
+    EvictedRange range;
+    range.seq = *cached[d.gpu].front().first;
+    range.tail_len = cached[d.gpu].front().second;
+    cached[d.gpu].pop_front();
+    s.note_eviction(range, d.gpu, now);
+  }
+}
+
+int main(int argc, char** argv) {
+  const int64_t n = argc > 1 ? std::atoll(argv[1]) : 3000;
+  WorkloadSpec spec = WorkloadSpec::archetype_default(Archetype::Toolbench);
+  spec.request_count = n;
+  Corpus corpus = generate(spec, 13);
+  assign_poisson_arrivals(corpus, 2000.0, 14);
+  const std::vector<Request> reqs = to_requests(corpus);
+  const int64_t trunk = spec.system_prompt_len + spec.branch_len;
+  SchedulerConfig cfg;
+  cfg.kv_capacity_tokens = 200000;
+  cfg.history_window_ms = 10000.0;
+  kvsched::GlobalScheduler ref(4, cfg, TimeModel{}, GlobalPolicy{});
+  kvsched::b200::GlobalScheduler dut(4, cfg, TimeModel{}, GlobalPolicy{});
+  std::vector<std::deque<std::pair<const TokenSeq*, int64_t>>> ca(4), cb(4);
+  SimTime now = 0;
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    const Request& r = reqs[i];
+    now = std::max(now, r.arrival_ms);
+    const Decision a = ref.schedule_request(r, now);
+    const Decision b = dut.schedule_request(r, now);
+    if (!same(a, b)) {
+      std::printf("MISMATCH at request %zu\n", i);
+      return 1;
+    }
+    step(ref, ca, r, now, trunk, a);
+    step(dut, cb, r, now, trunk, b);
+    if (i >= 2000) {
+      ref.note_finished(reqs[i - 2000].id, now, reqs[i - 2000].output_len);
+      dut.note_finished(reqs[i - 2000].id, now, reqs[i - 2000].output_len);
+    }
+  }
+  const GlobalStats sa = ref.stats(), sb = dut.stats();
+  if (sa.exploit != sb.exploit || sa.explore != sb.explore || sa.redirected != sb.redirected ||
+      sa.rebalance_installs != sb.rebalance_installs || sa.tree_reads != sb.tree_reads) {
+    std::printf("stats differ\n");
+    return 1;
+  }
+  std::printf("drop-in OK: %lld decisions identical (%s backend)\n", (long long)n, e2_backend());
+  return 0;
+}
