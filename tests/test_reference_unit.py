@@ -21,12 +21,12 @@ from paper_2407_00023_b200.scheduler import (
     TimeModel,
 )
 
-BACKENDS = ["ref", "hostsim", pytest.param("b200", marks=pytest.mark.gpu)]
+BACKENDS = ["ref", "oracle", "hostsim", pytest.param("b200", marks=pytest.mark.gpu)]
 
 
 @pytest.fixture(params=BACKENDS)
 def lib(request):
-    return request.getfixturevalue({"ref": "true_ref_lib", "hostsim": "hostsim_lib", "b200": "b200_lib"}[request.param])
+    return request.getfixturevalue({"ref": "true_ref_lib", "oracle": "oracle_lib", "hostsim": "hostsim_lib", "b200": "b200_lib"}[request.param])
 
 
 def identity():  # test_global_scheduler.cpp:11-18
