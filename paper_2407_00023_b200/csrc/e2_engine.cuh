@@ -603,9 +603,63 @@ E2_HD void inf_erase_at(u64 i) {
   DEV.inf[i].key = kNoInflight;
 }
 
-// commit (global_scheduler.cpp:160-175).  Warp-wide.  Returns the tail slot.
+// One bottom-up pass over the committed path: record_hit on every node
+// (prefix_tree.cpp:45-51, via insert :193-196) and, when `mark`,
+// mark_cached_path's set_cached + last_access update (:200-213) for the
+// same gpu and time.  In the batched driver note_prefill_cached follows the
+// commit immediately, so both passes are applied together; the LRU index is
+// a set, so moving each node once from its initial to its final
+// (membership, key) equals the reference's erase/insert sequence.  A node's
+// cached-child count is read before its child's increment is applied.
+// Returns the first-level node id.  Warp-wide.
+E2_DNI u64 path_update(u32 tail, int g, double now, bool mark) {
+  const int G = DEV.cfg.G;
+  bool inc = false;  // the previous (child) node became cached on g
+  u64 first_id = 0;
+  u32 v = tail;
+  while (v != kRoot) {
+    NodeRec* r = nget(v);
+    const u32 p = r->parent;
+    const u64 id = r->id;
+    const bool was = rcached(r, g);
+    const i32 ccc0 = rccc(r, G)[g];
+    const i32 ccc1 = ccc0 + (inc ? 1 : 0);
+    const double la0 = rla(r)[g];
+    const double la1 = now > la0 ? now : la0;
+    const bool newly = mark && !was;
+    const bool leaf0 = was && ccc0 == 0;
+    const bool leaf1 = (was || mark) && ccc1 == 0;
+    first_id = id;
+    if (lane0()) {
+      rhits(r, G)[g] += 1;
+      r->lamask |= (1ull << g);
+      rla(r)[g] = la1;
+      if (inc) rccc(r, G)[g] = ccc1;
+      if (newly) {
+        r->cmask |= (1ull << g);
+        HOT.cached_tokens[g] += r->edge_len;
+      }
+    }
+    wsync();
+    const bool moved = dbits(la0) != dbits(la1);
+    if (leaf0 && (!leaf1 || moved)) lru_erase(g, dbits(la0), id);
+    if (leaf1 && (!leaf0 || moved)) lru_insert(g, dbits(la1), id, v);
+    inc = newly;
+    v = p;
+  }
+  if (inc) {  // set_cached on a first-level node also counts on the root
+    NodeRec* r = nget(kRoot);
+    if (lane0()) rccc(r, G)[g] += 1;
+    wsync();
+  }
+  return first_id;
+}
+
+// commit (global_scheduler.cpp:160-175), optionally fused with the
+// driver's note_prefill_cached (see path_update).  Warp-wide.  Returns the
+// tail slot.
 E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
-                double now) {
+                  double now, bool mark) {
   if (DEV.cfg.mode == 1) {
     if (lane0()) HOT.rr_next++;
     wsync();
@@ -619,21 +673,7 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
   const u32 tail = ensure_path(seq_off, n, L, w);
   if (tail == kNil || HOT.err) return kNil;
   const int g = r.gpu;
-  const int G = DEV.cfg.G;
-  // record_hit bottom-up (prefix_tree.cpp:193-196)
-  u64 root_id = 0;
-  for (u32 v = tail; v != kRoot;) {
-    NodeRec* rv = nget(v);
-    const u32 p = rv->parent;
-    root_id = rv->id;
-    if (lane0()) {
-      rhits(rv, G)[g] += 1;
-      ndirty(rv);
-    }
-    wsync();
-    touch_la(v, g, now);
-    v = p;
-  }
+  const u64 root_id = path_update(tail, g, now, mark);
   if (lane0()) {
     win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail);
     HOT.inflight_cached[g] += r.cached_len;

@@ -221,7 +221,7 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
       Dec r = decide(s, seq, op.len, op.L, hint, kPathHint, op.now, w);
       if (!r.ok) return;
       if (commit_it) {
-        commit(op.off, op.len, op.L, w, r, op.id, op.arr, op.now);
+        commit(op.off, op.len, op.L, w, r, op.id, op.arr, op.now, false);
         if (HOT.err) return;
         count_stats(r);
       }
@@ -346,14 +346,15 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
   Walk w;
   Dec dec = decide(s, seq, n, a.L[li], a.hint + li * kPathHint, kPathHint, now, w);
   if (!dec.ok) return;
-  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now);
+  const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
+  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse);
   if (HOT.err) return;
   if (lane0()) DEV.req_tail[r] = tail;
   count_stats(dec);
   write_decision(s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
                  a.ratios ? a.ratios + r * G : nullptr);
   const int g = dec.gpu;
-  if (a.prefill && DEV.cfg.mode == 0) mark_cached_chain(tail, g, now);
+
   if (HOT.err) return;
   if (a.eviction == E2_EVICT_FIFO_TAIL) {
     if (lane0()) {
