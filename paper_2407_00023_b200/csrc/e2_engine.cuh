@@ -297,6 +297,25 @@ E2_DNI void cost_prepare(int g, i64 missed, double now) {
   if (missed - (DEV.cfg.cap - HOT.cached_tokens[g]) > 0) hits_catchup(g);
 }
 
+// Warp-wide, for every instance in `set` (missed = n - ext[g]): prune its
+// window and, only where the eviction term will be evaluated (need > 0),
+// bring its hit counters current.
+E2_DNI void cost_prepare_set(const Scr* s, u64 set, i64 n, double now) {
+  const int G = DEV.cfg.G;
+  u64 needm = 0;
+  for (int b = 0; b < G; b += kWidth) {
+    const int g = b + lane();
+    bool need = false;
+    if (g < G && ((set >> g) & 1ull)) {
+      win_prune(g, now);
+      need = (n - s->ext[g]) - (DEV.cfg.cap - HOT.cached_tokens[g]) > 0 && HOT.ws_done[g] < HOT.ws_head[g];
+    }
+    needm |= (u64)ballot(need) << b;
+  }
+  wsync();
+  for (u64 m = needm; m; m &= m - 1) hits_catchup(ffs64(m));
+}
+
 // ---------------------------------------------------------------------------
 // Walks (warp-wide).  `L` = matched length of the sequence against the
 // current tree, from the batched match; prefix_tree.cpp:79-114.  `hint`
@@ -319,19 +338,22 @@ E2_DNI Walk walk_known(const i32* seq, i64 L, const u32* hint, int nhint, i64* e
   while (pos < L) {
     const i32 t = seq[pos];
     u32 ch = kNil;
+    const NodeRec* r = nullptr;
     if (level < nhint) {
       const u32 c = hint[level];
       if (c != kNil) {
-        const NodeRec* rc = nget(c);
-        if (rc->parent == cur && rc->first_tok == t && rc->edge_len > 0) ch = c;
+        r = nget(c);
+        if (r->parent == cur && r->first_tok == t && r->edge_len > 0) ch = c;
       }
     }
-    if (ch == kNil) ch = child_lookup(cur, t);
     if (ch == kNil) {
-      w.ok = false;
-      break;
+      ch = child_lookup(cur, t);
+      if (ch == kNil) {
+        w.ok = false;
+        break;
+      }
+      r = nget(ch);
     }
-    const NodeRec* r = nget(ch);
     const i64 len = r->edge_len;
     const i64 m = min_(len, L - pos);
     const u64 cm = r->cmask;
@@ -483,16 +505,28 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
   if (r.missed_len < r.cached_len) {
     r.branch = 0;
     i64 best = 0;
-    for (u64 m = w.present; m; m &= m - 1) best = max_(best, s->ext[ffs64(m)]);
     u64 cand = 0;
+#if E2_DEVICE_BUILD
+    {
+      i64 mine = 0;
+      for (int g = lane(); g < G; g += kWidth)
+        if ((w.present >> g) & 1ull) mine = max_(mine, s->ext[g]);
+      for (int o = 16; o; o >>= 1) mine = max_(mine, (i64)__shfl_xor_sync(0xffffffffu, (long long)mine, o));
+      best = mine;
+      for (int b = 0; b < G; b += 32) {
+        const int g = b + lane();
+        const bool c = g < G && ((w.present >> g) & 1ull) && s->ext[g] == best;
+        cand |= (u64)ballot(c) << b;
+      }
+    }
+#else
+    for (u64 m = w.present; m; m &= m - 1) best = max_(best, s->ext[ffs64(m)]);
     for (u64 m = w.present; m; m &= m - 1) {
       const int g = ffs64(m);
       if (s->ext[g] == best) cand |= (1ull << g);
     }
-    for (u64 m = cand; m; m &= m - 1) {
-      const int g = ffs64(m);
-      cost_prepare(g, n - s->ext[g], now);
-    }
+#endif
+    cost_prepare_set(s, cand, n, now);
     for (int g = lane(); g < G; g += kWidth) {
       if ((cand >> g) & 1ull) {
         const int idx = popc64(cand & ((1ull << g) - 1));
@@ -543,7 +577,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
       r.gpu = max_g;
     } else {
       r.branch = 1;
-      for (int g = 0; g < G; ++g) cost_prepare(g, n - s->ext[g], now);
+      cost_prepare_set(s, G == 64 ? ~0ull : ((1ull << G) - 1), n, now);
       for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(g, n - s->ext[g], now));
       wsync();
       if (lane0()) s->n_costs = G;
@@ -817,6 +851,45 @@ E2_DNI i64 uncache_tail(u32 tail, i64 n, i64 tail_len, int g) {
   return clear_range_from(tail, start, g);
 }
 
+// Partial eviction of the last `tok` tokens of LRU leaf v on g
+// (uncache_suffix with the range ending at v's end: split at len-tok, clear
+// the suffix).  Net effect on g's LRU index: the leaf key (la, id) stays —
+// the prefix keeps v's id and last_access and becomes the leaf — so the
+// entry is relabelled to the prefix slot instead of erased and reinserted.
+// Other instances caching v see the suffix re-keyed exactly as in split.
+// Warp-wide.
+E2_DNI void evict_tail(u32 v, i64 tok, int g) {
+  const int G = DEV.cfg.G;
+  NodeRec* r = nget(v);
+  const u32 len = r->edge_len;
+  const u64 id0 = r->id, la0 = dbits(rla(r)[g]), cm = r->cmask;
+  const bool leaf = rleaf(r, v, g, G);
+  // other instances where v is a leaf: split re-keys them (new suffix id)
+  const u32 q = split_node(v, (u32)(len - tok), false);
+  if (q == kNil) return;
+  const u64 id1 = nget(v)->id;
+  for (u64 m = cm & ~(1ull << g); m; m &= m - 1) {
+    const int o = ffs64(m);
+    const NodeRec* rv = nget(v);
+    if (rccc(rv, G)[o] == 0) {
+      const u64 l = dbits(rla(rv)[o]);
+      lru_erase(o, l, id0);
+      lru_insert(o, l, id1, v);
+    }
+  }
+  // clear the suffix on g without touching g's index, then relabel
+  r = nget(v);
+  if (lane0()) {
+    r->cmask &= ~(1ull << g);
+    HOT.cached_tokens[g] -= r->edge_len;
+  }
+  wsync();
+  NodeRec* rq = nget(q);
+  if (lane0()) rccc(rq, G)[g] -= 1;  // 1 -> 0: the prefix is the leaf now
+  wsync();
+  if (leaf) lru_relabel(g, la0, id0, q);
+}
+
 // Mirror-LRU eviction: plan_eviction(g, over, {}, partial)
 // then note_eviction for every entry, ranges built before any is applied.
 E2_DNI void evict_lru(int g, i64 over) {
@@ -839,10 +912,10 @@ E2_DNI void evict_lru(int g, i64 over) {
     const u32 v = DEV.vic_slot[i];
     const i64 tok = DEV.vic_tok[i];
     const i64 len = nget(v)->edge_len;
-    if (tok < len) {
-      if (split_node(v, (u32)(len - tok)) == kNil) return;
-    }
-    clear_cached(v, g);
+    if (tok < len)
+      evict_tail(v, tok, g);
+    else
+      clear_cached(v, g);
   }
 }
 

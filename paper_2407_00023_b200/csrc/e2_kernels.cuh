@@ -333,26 +333,44 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
   }
 }
 
+#if defined(E2_PHASES) && E2_DEVICE_BUILD
+#define PHASE_T0() u64 _pt = clock64()
+#define PHASE(i)                                      \
+  do {                                                \
+    const u64 _pn = clock64();                        \
+    if (lane0()) HOT.phase_cycles[i] += _pn - _pt;    \
+    _pt = _pn;                                        \
+  } while (0)
+#else
+#define PHASE_T0()
+#define PHASE(i)
+#endif
+
 // One request of the generalised criterion-7 loop (e2sched.h, e2_replay).
 E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
   const int G = DEV.cfg.G;
   const i64 r = a.base + li;
   const i64 off = a.off[r], n = a.len[r];
   const i32* seq = DEV.tok + off;
+  PHASE_T0();
   const double now = max_(HOT.drv_now, a.arr[r]);
   if (lane0()) HOT.drv_now = now;
   wsync();
   if (DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, now);
+  PHASE(0);
   Walk w;
   Dec dec = decide(s, seq, n, a.L[li], a.hint + li * kPathHint, kPathHint, now, w);
   if (!dec.ok) return;
+  PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
   const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse);
   if (HOT.err) return;
+  PHASE(2);
   if (lane0()) DEV.req_tail[r] = tail;
   count_stats(dec);
   write_decision(s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
                  a.ratios ? a.ratios + r * G : nullptr);
+  PHASE(3);
   const int g = dec.gpu;
 
   if (HOT.err) return;
@@ -379,10 +397,12 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
     if (cached > a.hw && DEV.cfg.mode == 0) evict_lru(g, cached - a.hw);
   }
   if (HOT.err) return;
+  PHASE(4);
   if (li + a.base >= a.lag) {
     const i64 k = r - a.lag;
     note_finished(a.ids[k], now, a.outl[k]);
   }
+  PHASE(5);
 }
 
 E2_D void serial_body(Scr* s, const SerialArgs& a) {

@@ -1741,3 +1741,13 @@ int e2_profile_reset(e2_handle* h, int32_t enable_timing) {
 }
 
 }  // extern "C"
+
+#ifdef E2_PHASES
+// dev-only: per-phase cycle totals of the serial replay (E2_PHASES builds)
+extern "C" int e2_debug_phases(e2_handle* h, uint64_t* out) {
+  return guard(h, [&] {
+    pull_hot(h);
+    for (int i = 0; i < 8; ++i) out[i] = h->hot.phase_cycles[i];
+  });
+}
+#endif

@@ -589,6 +589,32 @@ E2_DNI void lru_erase(int g, u64 kla, u64 kid) {
   }
 }
 
+// warp-wide: the entry with key (kla, kid) now belongs to slot `slot`.
+E2_DNI void lru_relabel(int g, u64 kla, u64 kid, u32 slot) {
+  const u32 n = HOT.dir_n[g];
+  u32 k;
+  const DirEntry h0 = DEV.dir[dring(g, 0)];
+  if (n > 0 && !kless(h0.max_la, h0.max_id, kla, kid))
+    k = 0;
+  else
+    k = dir_lower_bound(g, kla, kid);
+  if (k >= n) {
+    if (lane0()) set_err(kErrSim, kWhyWalk);
+    wsync();
+    return;
+  }
+  const DirEntry e = k == 0 ? h0 : DEV.dir[dring(g, k)];
+  const u64 base = (u64)e.page * kPage;
+  const u32 m = vote(e.cnt, [&](int j) { return DEV.pg_la[base + j] == kla && DEV.pg_id[base + j] == kid; });
+  wsync();
+  if (!m) {
+    if (lane0()) set_err(kErrSim, kWhyWalk);
+  } else if (lane0()) {
+    DEV.pg_slot[base + ffs32(m)] = slot;
+  }
+  wsync();
+}
+
 // ---------------------------------------------------------------------------
 // Node state helpers (all warp-wide; records via the node cache)
 // ---------------------------------------------------------------------------
@@ -614,8 +640,9 @@ E2_D u32 node_alloc() {
 
 // warp-wide: split_node(s, k) with the slot kept on the suffix — see
 // e2_state.cuh.  Returns the new slot holding the prefix (old id).
-// Reference: prefix_tree.cpp:122-154.
-E2_DNI u32 split_node(u32 s, u32 k) {
+// Reference: prefix_tree.cpp:122-154.  rekey=false leaves the LRU index to
+// the caller (evict_tail: the suffix is uncached right away).
+E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
   const int G = DEV.cfg.G;
   NodeRec* rs = nget(s);
   const NodeRec hs = *rs;
@@ -654,6 +681,7 @@ E2_DNI u32 split_node(u32 s, u32 k) {
   wsync();
   child_update(hs.parent, hs.first_tok, q);
   child_insert(q, tok_k, s);
+  if (!rekey) return q;
   // LRU: the suffix inherits the leaf role under its new id.
   u64 m = hs.cmask;
   while (m) {
