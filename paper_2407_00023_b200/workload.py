@@ -108,6 +108,56 @@ class Config:
         return generate(s, self.seed, self.rps, self.arrival_seed, lib)
 
 
+def mix(traces, token_strides) -> Trace:
+    """Interleave several traces by arrival time (config 5's mixed workload).
+
+    Each component's token ids are shifted by its stride so unrelated
+    archetypes do not alias; ids stay int32 (the reference's TokenId)."""
+    parts = []
+    for t, stride in zip(traces, token_strides):
+        lens = np.diff(t.offsets)
+        toks = t.tokens.astype(np.int64) + stride
+        if toks.size and (toks.max() > np.iinfo(np.int32).max or toks.min() < 0):
+            raise ValueError("token id space exhausted by the mixture")
+        parts.append((t.arrivals, lens, toks.astype(np.int32), t.output_lens))
+    arr = np.concatenate([p[0] for p in parts])
+    order = np.argsort(arr, kind="stable")
+    lens = np.concatenate([p[1] for p in parts])
+    starts = np.concatenate([np.concatenate([[0], np.cumsum(p[1])[:-1]]) + sum(len(q[2]) for q in parts[:i])
+                             for i, p in enumerate(parts)])
+    toks_all = np.concatenate([p[2] for p in parts])
+    outl = np.concatenate([p[3] for p in parts])
+    n = len(arr)
+    new_off = np.zeros(n + 1, dtype=np.int64)
+    new_off[1:] = np.cumsum(lens[order])
+    tokens = np.empty(int(new_off[-1]), dtype=np.int32)
+    for k, i in enumerate(order):
+        tokens[new_off[k]:new_off[k + 1]] = toks_all[starts[i]:starts[i] + lens[i]]
+    return Trace(tokens, new_off, np.arange(1, n + 1, dtype=np.int64), arr[order].copy(), outl[order].copy())
+
+
+class MixConfig(Config):
+    """Config 5: toolbench + doc-QA + programming + tree-of-thought + embodied
+    chains, interleaved by arrival time, on 64 instances with a small cache
+    so the eviction term is active on most decisions."""
+
+    COMPONENTS = (("toolbench", 0.4, {}), ("doc_qa", 0.1, {}), ("programming", 0.2, {}),
+                  ("tree_of_thought", 0.2, {}), ("embodied_agent", 0.1, {}))
+
+    def trace(self, lib=None, n_requests: Optional[int] = None) -> Trace:
+        n = n_requests if n_requests is not None else self.n_requests
+        traces, strides = [], []
+        for k, (arch, frac, over) in enumerate(self.COMPONENTS):
+            s = default_spec(arch, lib)
+            s.request_count = max(1, int(round(n * frac)))
+            for a, v in over.items():
+                setattr(s, a, v)
+            traces.append(generate(s, self.seed + k, self.rps * frac, self.arrival_seed + k, lib))
+            strides.append(k * 20_000_000)
+        t = mix(traces, strides)
+        return t.head(min(n, t.n)) if t.n > n else t
+
+
 def _cs2_sched(cap=200000):
     # criterion-7 settings: cap 200000, H = 10 s (acceptance_main.cpp:380-383)
     return SchedulerConfig(kv_capacity_tokens=cap, history_window_ms=10000.0)
@@ -130,5 +180,16 @@ CONFIGS = {
         "c3_docqa_20k-40k_16inst", "doc_qa", 10000, 16, _cs2_sched(cap=100000),
         DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=90000, finish_lag=2000),
         spec_overrides=dict(branch_len=20000, branch_len_max=40000),
+    ),
+    # C4: tree-of-thought / programming-style deep branching: 64-request problems, fanout 3,
+    # depth <= 8 thought segments of 40-120 tokens; 1M requests (parity on prefixes).
+    "c4": Config(
+        "c4_tree_of_thought_1M_16inst", "tree_of_thought", 1_000_000, 16, _cs2_sched(cap=20000),
+        DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=19000, finish_lag=2000),
+    ),
+    # C5: mixed multi-workload, 10M requests, 64 instances, heavy eviction (cap 30k, high-water 0.95).
+    "c5": MixConfig(
+        "c5_mixed_10M_64inst", "mixed", 10_000_000, 64, _cs2_sched(cap=30000),
+        DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=28500, finish_lag=2000),
     ),
 }

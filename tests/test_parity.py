@@ -51,6 +51,9 @@ CASES = {
     "no_rebalance_no_pd": _cfg("nrb", "programming", 1200, 4, 30000, 20000, LRU,
                                policy=GlobalPolicy(rebalance=False, pd_balance=False)),
     "short_window": _cfg("shortH", "doc_qa", 1200, 8, 60000, 57000, LRU, H=300.0),
+    "c4_3k": dataclasses.replace(W.CONFIGS["c4"], n_requests=3000),
+    "c5_3k": W.MixConfig(**{f.name: getattr(W.CONFIGS["c5"], f.name) for f in dataclasses.fields(W.Config)
+                            if f.name != "n_requests"}, n_requests=3000),
 }
 
 
@@ -78,10 +81,11 @@ def test_replay_parity_b200(b200_lib, ref_lib, gen_lib, case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,n", [("c1", None), ("c2", None), ("c3", 3000)])
+@pytest.mark.parametrize("name,n", [("c1", None), ("c2", None), ("c3", 3000), ("c4", 20000), ("c5", 20000)])
 def test_full_config_parity_b200(b200_lib, ref_lib, gen_lib, name, n):
-    """BASELINE.json configs at full size (C3 on a prefix: the reference's
-    plan_eviction dominates its runtime)."""
+    """BASELINE.json configs: C1 and C2 at full size; C3-C5 on prefixes (the
+    reference's plan_eviction dominates its runtime, and C5's 10M requests
+    exceed one int32 token space without id reuse)."""
     cfg = W.CONFIGS[name]
     trace = cfg.trace(lib=gen_lib, n_requests=n)
     sa, a = replay(ref_lib, cfg, trace, want_ratios=False)
