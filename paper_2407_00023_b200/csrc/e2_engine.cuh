@@ -22,7 +22,13 @@ struct Scr {
   i32 cinf[kMaxG + 1];
   double cL[kMaxG + 1], cM[kMaxG + 1], cP[kMaxG + 1];
   i32 n_costs;
-  i32 pad;
+  i32 npath;  // levels recorded by walk_par (-1: path too deep, sequential fallback)
+  // the request's root path, top-down (walk_par / commit)
+  u32 pslot[kMaxPath + 1];
+  i64 pm[kMaxPath];  // tokens matched in the level
+  u64 pcm[kMaxPath];  // caching mask of the level
+  u64 pla0[kMaxPath + 1];  // path_update: old last_access bits
+  u32 pflag[kMaxPath + 1];  // path_update: bit0 newly cached, bit1 leaf before, bit2 leaf after, bit3 key moved
 };
 
 // Result of a node-level walk with a known matched length.
@@ -378,6 +384,219 @@ E2_DNI Walk walk_known(const i32* seq, i64 L, const u32* hint, int nhint, i64* e
   return w;
 }
 
+#if E2_DEVICE_BUILD
+E2_D i64 warp_incl_sum(i64 v) {
+  for (int o = 1; o < 32; o <<= 1) {
+    const i64 u = (i64)__shfl_up_sync(0xffffffffu, (long long)v, o);
+    if (lane() >= o) v += u;
+  }
+  return v;
+}
+E2_D i64 warp_sum(i64 v) {
+  for (int o = 16; o; o >>= 1) v += (i64)__shfl_xor_sync(0xffffffffu, (long long)v, o);
+  return v;
+}
+#endif
+
+// Walk with a known matched length, level-parallel (warp-wide): 32 hinted
+// levels are loaded and validated at once (parent chain, first token,
+// position from a prefix sum of edge lengths); levels without a valid hint
+// fall back to one child-table probe each.  Records the path top-down in
+// s->pslot/pm/pcm and derives the per-gpu extents and cached_len from it
+// (prefix_tree.cpp:79-114).  s->npath = -1 when the path exceeds kMaxPath:
+// the caller then uses the sequential walk.
+E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) {
+  Walk w;
+  w.last = kRoot;
+  w.last_m = 0;
+  w.cached_len = 0;
+  w.present = 0;
+  w.ok = true;
+  const int G = DEV.cfg.G;
+  int np = 0;
+  i64 pos = 0;
+  u32 cur = kRoot;
+  bool fast = hint != nullptr;
+  bool done = false;
+  while (pos < L && !done) {
+    if (np >= kMaxPath) {
+      if (lane0()) s->npath = -1;
+      wsync();
+      w.ok = false;
+      return w;
+    }
+#if E2_DEVICE_BUILD
+    if (fast && np < nhint) {
+      const int k = lane(), lvl = np + k;
+      bool in = lvl < nhint && lvl < kMaxPath;
+      const u32 c = in ? hint[lvl] : kNil;
+      in = in && c != kNil;
+      u32 par = kNil;
+      i32 ft = 0;
+      i64 len = 0;
+      u64 cm = 0;
+      if (in) {
+        const NodeRec* r = npeek(c);
+        par = r->parent;
+        ft = r->first_tok;
+        len = r->edge_len;
+        cm = r->cmask;
+      }
+      const i64 pk = pos + warp_incl_sum(len) - len;
+      u32 prev = __shfl_up_sync(0xffffffffu, c, 1);
+      if (k == 0) prev = cur;
+      const bool ok = in && par == prev && len > 0 && pk < L && seq[pk] == ft;
+      const u32 okm = ballot(ok);
+      const int nvalid = (okm == 0xffffffffu) ? 32 : ffs32(~okm);
+      const u32 lastm = ballot(ok && pk + len >= L) & (nvalid == 32 ? 0xffffffffu : ((1u << nvalid) - 1));
+      const int used = lastm ? ffs32(lastm) + 1 : nvalid;
+      if (used == 0) {
+        fast = false;
+        continue;
+      }
+      const i64 m = min_(len, L - pk);
+      if (k < used) {
+        s->pslot[np + k] = c;
+        s->pm[np + k] = m;
+        s->pcm[np + k] = cm;
+      }
+      const u32 lc = shfl(c, used - 1);
+      const i64 lm = shfl(m, used - 1), lp = shfl(pk, used - 1), ll = shfl(len, used - 1);
+      wsync();
+      np += used;
+      pos = lp + lm;
+      cur = lc;
+      w.last = lc;
+      w.last_m = lm;
+      if (lastm) done = true;  // reached L (or the match ends inside this edge)
+      if (lm < ll) done = true;
+      if (used < 32) fast = false;
+      continue;
+    }
+#endif
+    const i32 t = seq[pos];
+    u32 ch = kNil;
+    const NodeRec* r = nullptr;
+    if (fast && np < nhint) {
+      const u32 c = hint[np];
+      if (c != kNil) {
+        r = nget(c);
+        if (r->parent == cur && r->first_tok == t && r->edge_len > 0) ch = c;
+      }
+    }
+    if (ch == kNil) {
+      fast = false;
+      ch = child_lookup(cur, t);
+      if (ch == kNil) {
+        w.ok = false;
+        break;
+      }
+      r = nget(ch);
+    }
+    const i64 len = r->edge_len;
+    const i64 m = min_(len, L - pos);
+    const u64 cm = r->cmask;
+    if (lane0()) {
+      s->pslot[np] = ch;
+      s->pm[np] = m;
+      s->pcm[np] = cm;
+    }
+    wsync();
+    np++;
+    pos += m;
+    cur = ch;
+    w.last = ch;
+    w.last_m = m;
+    if (m < len) break;
+  }
+  if (lane0()) s->npath = np;
+  wsync();
+  if (!w.ok) return w;
+  // extents: a gpu accumulates while every level so far is cached on it;
+  // entries exist for the gpus caching the first span
+  w.present = np > 0 ? s->pcm[0] : 0;
+  for (int g = lane(); g < G; g += kWidth) {
+    i64 e = 0;
+    if ((w.present >> g) & 1ull)
+      for (int l = 0; l < np && ((s->pcm[l] >> g) & 1ull); ++l) e += s->pm[l];
+    s->ext[g] = e;
+  }
+  i64 cl = 0;
+  for (int l = lane(); l < np; l += kWidth)
+    if (s->pcm[l] != 0) cl += s->pm[l];
+#if E2_DEVICE_BUILD
+  cl = warp_sum(cl);
+#endif
+  w.cached_len = cl;
+  wsync();
+  return w;
+}
+
+// path_update over the recorded path (s->pslot[0..D), top-down), one lane
+// per node: same final state as the sequential path_update.  Nodes whose
+// LRU membership or key changes are re-indexed afterwards, serially.
+// Warp-wide.
+E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark) {
+  const int G = DEV.cfg.G;
+  // pass 1: which nodes become cached (a parent's count uses its child's flag)
+  for (int i = lane(); i < D; i += kWidth) {
+    const NodeRec* r = npeek(s->pslot[i]);
+    s->pflag[i] = (mark && !rcached(r, g)) ? 1u : 0u;
+  }
+  wsync();
+  i64 add = 0;
+  u32 any = 0;
+  for (int i = lane(); i < D; i += kWidth) {
+    NodeRec* r = npoke(s->pslot[i]);
+    const bool newly = s->pflag[i] & 1u;
+    const bool inc = i + 1 < D && (s->pflag[i + 1] & 1u);
+    const bool was = rcached(r, g);
+    const i32 ccc0 = rccc(r, G)[g];
+    const i32 ccc1 = ccc0 + (inc ? 1 : 0);
+    const double la0 = rla(r)[g];
+    const double la1 = now > la0 ? now : la0;
+    const bool leaf0 = was && ccc0 == 0;
+    const bool leaf1 = (was || mark) && ccc1 == 0;
+    const bool moved = dbits(la0) != dbits(la1);
+    rhits(r, G)[g] += 1;
+    r->lamask |= (1ull << g);
+    rla(r)[g] = la1;
+    if (inc) rccc(r, G)[g] = ccc1;
+    if (newly) {
+      r->cmask |= (1ull << g);
+      add += r->edge_len;
+    }
+    const bool fix = (leaf0 && (!leaf1 || moved)) || (leaf1 && (!leaf0 || moved));
+    s->pla0[i] = dbits(la0);
+    s->pflag[i] = (newly ? 1u : 0u) | (leaf0 ? 2u : 0u) | (leaf1 ? 4u : 0u) | (fix ? 8u : 0u);
+    any |= fix ? 1u : 0u;
+  }
+#if E2_DEVICE_BUILD
+  add = warp_sum(add);
+  any = ballot(any != 0) ? 1u : 0u;
+#endif
+  wsync();
+  if (lane0()) HOT.cached_tokens[g] += add;
+  wsync();
+  if (D > 0 && (s->pflag[0] & 1u)) {  // a first-level node became cached: root count
+    NodeRec* r = nget(kRoot);
+    if (lane0()) rccc(r, G)[g] += 1;
+    wsync();
+  }
+  if (any) {
+    for (int i = 0; i < D; ++i) {
+      const u32 f = s->pflag[i];
+      if (!(f & 8u)) continue;
+      const u32 v = s->pslot[i];
+      const NodeRec* r = nget(v);
+      const u64 id = r->id, la1 = dbits(rla(r)[g]);
+      if (f & 2u) lru_erase(g, s->pla0[i], id);
+      if (f & 4u) lru_insert(g, la1, id, v);
+    }
+  }
+  return D > 0 ? nget(s->pslot[0])->id : 0;
+}
+
 // ensure_path (prefix_tree.cpp:156-185) given the walk of the same sequence.
 // Returns the node whose edge ends exactly at |seq| (kNil on error).
 E2_DNI u32 ensure_path(i64 seq_off, i64 n, i64 L, const Walk& w) {
@@ -489,7 +708,8 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
   }
   if (lane0()) HOT.stats[kStTreeReads]++;
   wsync();
-  w = walk_known(seq, L, hint, nhint, s->ext);
+  w = walk_par(seq, L, hint, nhint, s);
+  if (!w.ok && s->npath < 0) w = walk_known(seq, L, hint, nhint, s->ext);
   if (!w.ok) {
     if (lane0()) set_err(kErrSim, kWhyWalk);
     wsync();
@@ -693,7 +913,7 @@ E2_DNI u64 path_update(u32 tail, int g, double now, bool mark) {
 // driver's note_prefill_cached (see path_update).  Warp-wide.  Returns the
 // tail slot.
 E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
-                  double now, bool mark) {
+                  double now, bool mark, Scr* s_path) {
   if (DEV.cfg.mode == 1) {
     if (lane0()) HOT.rr_next++;
     wsync();
@@ -707,7 +927,30 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
   const u32 tail = ensure_path(seq_off, n, L, w);
   if (tail == kNil || HOT.err) return kNil;
   const int g = r.gpu;
-  const u64 root_id = path_update(tail, g, now, mark);
+  u64 root_id;
+  int D = s_path ? s_path->npath : -1;
+  if (D >= 0) {
+    // the path after ensure_path: the split prefix (or the last level)
+    // ends at L; a new leaf is appended when L < n
+    const u32 at_L = (L == n) ? tail : (L > 0 ? nget(tail)->parent : kNil);
+    if (L > 0 && D > 0) {
+      if (lane0()) s_path->pslot[D - 1] = at_L;
+      wsync();
+    }
+    if (L < n) {
+      if (D + 1 > kMaxPath) {
+        D = -1;
+      } else {
+        if (lane0()) s_path->pslot[D] = tail;
+        wsync();
+        D++;
+      }
+    }
+  }
+  if (D >= 0)
+    root_id = path_update_par(s_path, D, g, now, mark);
+  else
+    root_id = path_update(tail, g, now, mark);
   if (lane0()) {
     win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail);
     HOT.inflight_cached[g] += r.cached_len;

@@ -221,7 +221,7 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
       Dec r = decide(s, seq, op.len, op.L, hint, kPathHint, op.now, w);
       if (!r.ok) return;
       if (commit_it) {
-        commit(op.off, op.len, op.L, w, r, op.id, op.arr, op.now, false);
+        commit(op.off, op.len, op.L, w, r, op.id, op.arr, op.now, false, s);
         if (HOT.err) return;
         count_stats(r);
       }
@@ -363,7 +363,7 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
   if (!dec.ok) return;
   PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
-  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse);
+  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s);
   if (HOT.err) return;
   PHASE(2);
   if (lane0()) DEV.req_tail[r] = tail;

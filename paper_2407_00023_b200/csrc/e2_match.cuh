@@ -83,8 +83,8 @@ E2_D MatchRes match_one(const i32* seq, i64 n, u32* path) {
     r.div_m = (u32)m;
     if (m < len) break;
   }
-  if (path && lane0())
-    for (int l = level; l < kPathHint; ++l) path[l] = kNil;
+  if (path)
+    for (int l = level + lane(); l < kPathHint; l += kWidth) path[l] = kNil;
   r.S = pos;
   // B_match = 4*min(|p|, matched+1) + 4*matched + 32*(depth+1)
   r.bytes = 4 * min_(n, pos + 1) + 4 * pos + 32 * (depth + 1);

@@ -93,7 +93,8 @@ constexpr u64 kEmptyKey = ~0ull;
 constexpr u64 kTombKey = ~0ull - 1;
 constexpr i64 kNoInflight = INT64_MIN;
 constexpr int kPage = 32;   // LRU keys per page
-constexpr int kPathHint = 8;  // path slots K1 records per request
+constexpr int kPathHint = 64;  // path slots K1 records per request
+constexpr int kMaxPath = 256;  // levels a request keeps in shared memory
 
 // Error codes mirrored from e2sched.h.
 constexpr i32 kErrConfig = 1;

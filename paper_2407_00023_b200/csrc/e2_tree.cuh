@@ -140,6 +140,15 @@ E2_HD const NodeRec* npeek(u32 s) {
   return grec(s);
 }
 
+// single-lane writable view: the cached copy if resident, else HBM.  Only
+// for phases without cache fills (each lane touching a different node).
+E2_HD NodeRec* npoke(u32 s) {
+  const u32 base = (s & (NC.nsets - 1)) * kWays;
+  for (u32 k = 0; k < (u32)kWays; ++k)
+    if (NC.tag[base + k] == s) return nentry(base + k);
+  return grec(s);
+}
+
 // warp-wide: write every dirty record back.
 E2_D void nflush() {
   const u32 n = NC.nsets * kWays;
