@@ -25,11 +25,20 @@ struct Scr {
   i32 npath;  // levels recorded by walk_par (-1: path too deep, sequential fallback)
   // the request's root path, top-down (walk_par / commit)
   u32 pslot[kMaxPath + 1];
-  i64 pm[kMaxPath];  // tokens matched in the level
+  u32 pm[kMaxPath];  // tokens matched in the level
   u64 pcm[kMaxPath];  // caching mask of the level
   u64 pla0[kMaxPath + 1];  // path_update: old last_access bits
   u32 pflag[kMaxPath + 1];  // path_update: bit0 newly cached, bit1 leaf before, bit2 leaf after, bit3 key moved
 };
+
+// Per-level path arrays: levels [0, kMaxPath) in shared memory (Scr),
+// deeper ones in the handle's global overflow; max depth kMaxPath + kXPath.
+#define PSLOT(s, i) (*((i) < kMaxPath ? &(s)->pslot[(i)] : &DEV.xp_slot[(i)-kMaxPath]))
+#define PM(s, i) (*((i) < kMaxPath ? &(s)->pm[(i)] : &DEV.xp_m[(i)-kMaxPath]))
+#define PCM(s, i) (*((i) < kMaxPath ? &(s)->pcm[(i)] : &DEV.xp_cm[(i)-kMaxPath]))
+#define PLA0(s, i) (*((i) < kMaxPath ? &(s)->pla0[(i)] : &DEV.xp_la0[(i)-kMaxPath]))
+#define PFLAG(s, i) (*((i) < kMaxPath ? &(s)->pflag[(i)] : &DEV.xp_flag[(i)-kMaxPath]))
+constexpr int kPathLevels = kMaxPath + (int)kXPath;
 
 // Result of a node-level walk with a known matched length.
 struct Walk {
@@ -92,7 +101,7 @@ E2_HD double win_load(int g, double now) {
   return dadd(prefill, decode);
 }
 
-E2_HD bool win_add_sched(int g, double now, i64 missed, i64 est, u32 tail) {
+E2_HD bool win_add_sched(int g, double now, i64 missed, i64 est, u32 tail, u32 plen) {
   const u64 t = HOT.ws_tail[g];
   if (t - HOT.ws_done[g] >= DEV.wcap) {
     set_err(kErrCapacity, kWhyWindowCap);
@@ -103,7 +112,7 @@ E2_HD bool win_add_sched(int g, double now, i64 missed, i64 est, u32 tail) {
   e.missed = missed;
   e.est = est;
   e.slot = tail;
-  e.pad = 0;
+  e.plen = plen;
   DEV.win[wslot(g, t)] = e;
   if (t == HOT.ws_head[g]) HOT.ws_head_t[g] = now;
   HOT.ws_tail[g] = t + 1;
@@ -130,26 +139,63 @@ E2_HD bool win_add_comp(int g, double now, i64 out) {
 
 // hits(n, g) counts in-window requests placed on g whose prompt passes
 // through n.  Undo the stamps of requests that left g's
-// window since the last catch-up, walking each one's path from its tail
-// slot (splits since then put the copied stamps on the new prefix nodes,
-// which the parent walk visits too).  Warp-wide.
+// window since the last catch-up.  A logged entry's path (top-down slots
+// at commit) is decremented level-parallel; splits since then inserted
+// prefix nodes above some logged slots (they copied the stamp), found as
+// the parent chain between consecutive logged slots.  Unlogged entries walk
+// the parent chain from their tail slot.  Warp-wide.
 E2_DNI void hits_catchup(int g) {
   const int G = DEV.cfg.G;
   while (HOT.ws_done[g] < HOT.ws_head[g]) {
-    const u32 tail = DEV.win[wslot(g, HOT.ws_done[g])].slot;
-    for (u32 n = tail; n != kRoot && n != kNil;) {
-      NodeRec* r = nget(n);
-      const u32 p = r->parent;
-      if (lane0()) {
-        rhits(r, G)[g] -= 1;
-        ndirty(r);
+    const WinEnt e = DEV.win[wslot(g, HOT.ws_done[g])];
+    if (e.plen != kNil) {
+      const u64 h0 = HOT.pl_head[g], pmask = DEV.pcap - 1;
+      const u32* ring = DEV.plog + (u64)g * DEV.pcap;
+      for (u32 b = 0; b < e.plen; b += kWidth) {
+        const u32 i = b + (u32)lane();
+        if (i < e.plen) {
+          const u32 v = ring[(h0 + i) & pmask];
+          const u32 up = i == 0 ? kRoot : ring[(h0 + i - 1) & pmask];
+          NodeRec* r = npoke(v);
+          rhits(r, G)[g] -= 1;
+          for (u32 p = r->parent; p != up && p != kRoot && p != kNil;) {
+            NodeRec* rp = npoke(p);
+            rhits(rp, G)[g] -= 1;
+            p = rp->parent;
+          }
+        }
       }
       wsync();
-      n = p;
+      if (lane0()) HOT.pl_head[g] = h0 + e.plen;
+    } else {
+      for (u32 n = e.slot; n != kRoot && n != kNil;) {
+        NodeRec* r = nget(n);
+        const u32 p = r->parent;
+        if (lane0()) {
+          rhits(r, G)[g] -= 1;
+          ndirty(r);
+        }
+        wsync();
+        n = p;
+      }
     }
     if (lane0()) HOT.ws_done[g]++;
     wsync();
   }
+}
+
+// Append a committed path (top-down slots) to g's path log; returns the
+// logged length, or kNil when the ring has no room (the entry then falls
+// back to the parent-chain walk).  Warp-wide.
+E2_DNI u32 plog_append(Scr* s, int D, int g) {
+  const u64 t = HOT.pl_tail[g];
+  if (D < 0 || DEV.pcap == 0 || t + (u64)D - HOT.pl_head[g] > DEV.pcap) return kNil;
+  u32* ring = DEV.plog + (u64)g * DEV.pcap;
+  for (int i = lane(); i < D; i += kWidth) ring[(t + (u64)i) & (DEV.pcap - 1)] = PSLOT(s, i);
+  wsync();
+  if (lane0()) HOT.pl_tail[g] = t + (u64)D;
+  wsync();
+  return (u32)D;
 }
 
 E2_HD double prefill_time(const Cfg& c, i64 missed) {
@@ -341,15 +387,18 @@ E2_DNI Walk walk_known(const i32* seq, i64 L, const u32* hint, int nhint, i64* e
   i64 pos = 0;
   u32 cur = kRoot;
   int level = 0;
+  bool live = hint != nullptr;  // hints end at K1's kNil terminator
   while (pos < L) {
     const i32 t = seq[pos];
     u32 ch = kNil;
     const NodeRec* r = nullptr;
-    if (level < nhint) {
+    if (live && level < nhint) {
       const u32 c = hint[level];
       if (c != kNil) {
         r = nget(c);
         if (r->parent == cur && r->first_tok == t && r->edge_len > 0) ch = c;
+      } else {
+        live = false;
       }
     }
     if (ch == kNil) {
@@ -419,7 +468,7 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
   bool fast = hint != nullptr;
   bool done = false;
   while (pos < L && !done) {
-    if (np >= kMaxPath) {
+    if (np >= kPathLevels) {
       if (lane0()) s->npath = -1;
       wsync();
       w.ok = false;
@@ -428,9 +477,11 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
 #if E2_DEVICE_BUILD
     if (fast && np < nhint) {
       const int k = lane(), lvl = np + k;
-      bool in = lvl < nhint && lvl < kMaxPath;
+      bool in = lvl < nhint && lvl < kPathLevels;
       const u32 c = in ? hint[lvl] : kNil;
-      in = in && c != kNil;
+      // K1 terminates the hint list with kNil; nothing after it is read
+      const u32 nilm = ballot(c == kNil);
+      in = k < (nilm ? ffs32(nilm) : 32);
       u32 par = kNil;
       i32 ft = 0;
       i64 len = 0;
@@ -456,9 +507,9 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
       }
       const i64 m = min_(len, L - pk);
       if (k < used) {
-        s->pslot[np + k] = c;
-        s->pm[np + k] = m;
-        s->pcm[np + k] = cm;
+        PSLOT(s, np + k) = c;
+        PM(s, np + k) = (u32)m;
+        PCM(s, np + k) = cm;
       }
       const u32 lc = shfl(c, used - 1);
       const i64 lm = shfl(m, used - 1), lp = shfl(pk, used - 1), ll = shfl(len, used - 1);
@@ -497,9 +548,9 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
     const i64 m = min_(len, L - pos);
     const u64 cm = r->cmask;
     if (lane0()) {
-      s->pslot[np] = ch;
-      s->pm[np] = m;
-      s->pcm[np] = cm;
+      PSLOT(s, np) = ch;
+      PM(s, np) = (u32)m;
+      PCM(s, np) = cm;
     }
     wsync();
     np++;
@@ -514,16 +565,46 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
   if (!w.ok) return w;
   // extents: a gpu accumulates while every level so far is cached on it;
   // entries exist for the gpus caching the first span
-  w.present = np > 0 ? s->pcm[0] : 0;
+  w.present = np > 0 ? PCM(s, 0) : 0;
+#if E2_DEVICE_BUILD
+  // level-parallel: alive_l = AND of pcm[0..l] (monotone), P_l = matched
+  // tokens through level l; gpu g's extent is P at the last level where it
+  // is alive, written by the lane of the level where it drops out.
+  for (int g = lane(); g < G; g += kWidth) s->ext[g] = 0;
+  wsync();
+  {
+    u64 carry = ~0ull;
+    i64 pcarry = 0;
+    for (int b = 0; b < np; b += kWidth) {
+      const int l = b + lane();
+      const bool in = l < np;
+      u64 v = in ? PCM(s, l) : ~0ull;
+      for (int o = 1; o < 32; o <<= 1) {
+        const u64 u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane() >= o) v &= u;
+      }
+      v &= carry;
+      const i64 P = pcarry + warp_incl_sum(in ? (i64)PM(s, l) : 0);
+      const u64 dn = __shfl_down_sync(0xffffffffu, v, 1);
+      const u64 an = (l + 1 < np) ? (lane() < 31 ? dn : (v & PCM(s, l + 1))) : 0ull;
+      if (in)
+        for (u64 d = v & ~an; d; d &= d - 1) s->ext[ffs64(d)] = P;
+      carry = shfl(v, 31);
+      pcarry = shfl(P, 31);
+    }
+  }
+  wsync();
+#else
   for (int g = lane(); g < G; g += kWidth) {
     i64 e = 0;
     if ((w.present >> g) & 1ull)
-      for (int l = 0; l < np && ((s->pcm[l] >> g) & 1ull); ++l) e += s->pm[l];
+      for (int l = 0; l < np && ((PCM(s, l) >> g) & 1ull); ++l) e += PM(s, l);
     s->ext[g] = e;
   }
+#endif
   i64 cl = 0;
   for (int l = lane(); l < np; l += kWidth)
-    if (s->pcm[l] != 0) cl += s->pm[l];
+    if (PCM(s, l) != 0) cl += (i64)PM(s, l);
 #if E2_DEVICE_BUILD
   cl = warp_sum(cl);
 #endif
@@ -540,16 +621,16 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark) {
   const int G = DEV.cfg.G;
   // pass 1: which nodes become cached (a parent's count uses its child's flag)
   for (int i = lane(); i < D; i += kWidth) {
-    const NodeRec* r = npeek(s->pslot[i]);
-    s->pflag[i] = (mark && !rcached(r, g)) ? 1u : 0u;
+    const NodeRec* r = npeek(PSLOT(s, i));
+    PFLAG(s, i) = (mark && !rcached(r, g)) ? 1u : 0u;
   }
   wsync();
   i64 add = 0;
   u32 any = 0;
   for (int i = lane(); i < D; i += kWidth) {
-    NodeRec* r = npoke(s->pslot[i]);
-    const bool newly = s->pflag[i] & 1u;
-    const bool inc = i + 1 < D && (s->pflag[i + 1] & 1u);
+    NodeRec* r = npoke(PSLOT(s, i));
+    const bool newly = PFLAG(s, i) & 1u;
+    const bool inc = i + 1 < D && (PFLAG(s, i + 1) & 1u);
     const bool was = rcached(r, g);
     const i32 ccc0 = rccc(r, G)[g];
     const i32 ccc1 = ccc0 + (inc ? 1 : 0);
@@ -567,8 +648,8 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark) {
       add += r->edge_len;
     }
     const bool fix = (leaf0 && (!leaf1 || moved)) || (leaf1 && (!leaf0 || moved));
-    s->pla0[i] = dbits(la0);
-    s->pflag[i] = (newly ? 1u : 0u) | (leaf0 ? 2u : 0u) | (leaf1 ? 4u : 0u) | (fix ? 8u : 0u);
+    PLA0(s, i) = dbits(la0);
+    PFLAG(s, i) = (newly ? 1u : 0u) | (leaf0 ? 2u : 0u) | (leaf1 ? 4u : 0u) | (fix ? 8u : 0u);
     any |= fix ? 1u : 0u;
   }
 #if E2_DEVICE_BUILD
@@ -578,23 +659,23 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark) {
   wsync();
   if (lane0()) HOT.cached_tokens[g] += add;
   wsync();
-  if (D > 0 && (s->pflag[0] & 1u)) {  // a first-level node became cached: root count
+  if (D > 0 && (PFLAG(s, 0) & 1u)) {  // a first-level node became cached: root count
     NodeRec* r = nget(kRoot);
     if (lane0()) rccc(r, G)[g] += 1;
     wsync();
   }
   if (any) {
     for (int i = 0; i < D; ++i) {
-      const u32 f = s->pflag[i];
+      const u32 f = PFLAG(s, i);
       if (!(f & 8u)) continue;
-      const u32 v = s->pslot[i];
+      const u32 v = PSLOT(s, i);
       const NodeRec* r = nget(v);
       const u64 id = r->id, la1 = dbits(rla(r)[g]);
-      if (f & 2u) lru_erase(g, s->pla0[i], id);
+      if (f & 2u) lru_erase(g, PLA0(s, i), id);
       if (f & 4u) lru_insert(g, la1, id, v);
     }
   }
-  return D > 0 ? nget(s->pslot[0])->id : 0;
+  return D > 0 ? nget(PSLOT(s, 0))->id : 0;
 }
 
 // ensure_path (prefix_tree.cpp:156-185) given the walk of the same sequence.
@@ -934,25 +1015,28 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
     // ends at L; a new leaf is appended when L < n
     const u32 at_L = (L == n) ? tail : (L > 0 ? nget(tail)->parent : kNil);
     if (L > 0 && D > 0) {
-      if (lane0()) s_path->pslot[D - 1] = at_L;
+      if (lane0()) PSLOT(s_path, D - 1) = at_L;
       wsync();
     }
     if (L < n) {
-      if (D + 1 > kMaxPath) {
+      if (D + 1 > kPathLevels) {
         D = -1;
       } else {
-        if (lane0()) s_path->pslot[D] = tail;
+        if (lane0()) PSLOT(s_path, D) = tail;
         wsync();
         D++;
       }
     }
   }
-  if (D >= 0)
+  u32 plen = kNil;
+  if (D >= 0) {
     root_id = path_update_par(s_path, D, g, now, mark);
-  else
+    plen = plog_append(s_path, D, g);
+  } else {
     root_id = path_update(tail, g, now, mark);
+  }
   if (lane0()) {
-    win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail);
+    win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail, plen);
     HOT.inflight_cached[g] += r.cached_len;
     HOT.inflight_prompt[g] += n;
     bool found;

@@ -59,7 +59,9 @@ struct SerialArgs {
   const double* arr;
   const i64* outl;
   const i64* L;     // batch-local
-  const u32* hint;  // batch-local K1 path hints [n][kPathHint]
+  const u32* hint;  // batch-local K1 path hints [n][hstride]
+  i32 hstride;
+  i32 pad2;
   e2_decision* dec;
   e2_cost* costs;
   double* ratios;
@@ -209,7 +211,7 @@ E2_D void subtree_apply(u32 root, int g, double now, bool mark) {
   }
 }
 
-E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
+E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, int nh, ApiOut* out) {
   const int G = DEV.cfg.G;
   const i32* seq = DEV.tok + op.off;
   switch (op.kind) {
@@ -218,7 +220,7 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
       const bool commit_it = op.kind == OP_SCHEDULE;
       if (commit_it && DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, op.now);
       Walk w;
-      Dec r = decide(s, seq, op.len, op.L, hint, kPathHint, op.now, w);
+      Dec r = decide(s, seq, op.len, op.L, hint, nh, op.now, w);
       if (!r.ok) return;
       if (commit_it) {
         commit(op.off, op.len, op.L, w, r, op.id, op.arr, op.now, false, s);
@@ -230,7 +232,7 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
     }
     case OP_PREFILL: {
       if (DEV.cfg.mode != 0 || op.len == 0) break;
-      Walk w = walk_known(seq, op.L, hint, kPathHint, s->ext);
+      Walk w = walk_known(seq, op.L, hint, nh, s->ext);
       if (!w.ok) {
         if (lane0()) set_err(kErrSim, kWhyWalk);
         wsync();
@@ -270,7 +272,7 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, ApiOut* out) {
       break;
     }
     case OP_MATCH: {
-      Walk w = walk_known(seq, op.L, hint, kPathHint, s->ext);
+      Walk w = walk_known(seq, op.L, hint, nh, s->ext);
       for (int g = lane(); g < G; g += kWidth) out->ext[g] = ((w.present >> g) & 1ull) ? s->ext[g] : 0;
       if (lane0()) {
         out->i0 = op.L;
@@ -359,7 +361,7 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
   if (DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, now);
   PHASE(0);
   Walk w;
-  Dec dec = decide(s, seq, n, a.L[li], a.hint + li * kPathHint, kPathHint, now, w);
+  Dec dec = decide(s, seq, n, a.L[li], a.hint + li * a.hstride, a.hstride, now, w);
   if (!dec.ok) return;
   PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
@@ -421,7 +423,7 @@ E2_D void serial_body(Scr* s, const SerialArgs& a) {
     if (lane0()) HOT.done = i;
     wsync();
   } else {
-    api_op(s, a.op, a.hint, a.out);
+    api_op(s, a.op, a.hint, a.hstride, a.out);
     if (lane0()) HOT.done = HOT.err ? 0 : 1;
     wsync();
   }

@@ -158,16 +158,19 @@ __global__ void __launch_bounds__(32, 1) k_serial(SerialArgs a, u32 nsets) {
 
 __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32) k_match(i64 n, i64 base, const i64* off,
                                                                      const i64* len, i64* S, u32* dslot, u32* dm,
-                                                                     u32* path, unsigned long long* bytes) {
+                                                                     u32* path, int hstride,
+                                                                     unsigned long long* bytes,
+                                                                     unsigned int* max_levels) {
   const i64 w = (i64)blockIdx.x * kMatchWarpsPerBlock + (threadIdx.x >> 5);
   if (w >= n) return;
   const i64 r = base + w;
-  MatchRes m = match_one(g_dev.tok + off[r], len[r], path + w * kPathHint);
+  MatchRes m = match_one(g_dev.tok + off[r], len[r], path + w * hstride, hstride);
   if (lane0()) {
     S[w] = m.S;
     dslot[w] = m.div_slot;
     dm[w] = m.div_m;
     atomicAdd(bytes, (unsigned long long)m.bytes);
+    if (m.levels >= hstride) atomicMax(max_levels, (unsigned int)min_<i64>(m.levels, 0x7fffffff));
   }
 }
 
@@ -301,7 +304,9 @@ struct e2_handle {
   u64* g_tk = nullptr;
   u32* g_tv = nullptr;
   u64 g_mask = 0;
-  unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions
+  unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions, [2] deepest K1 path beyond the hint stride
+  int hstride = kPathHint;             // K1 path hints per request (grown when paths get deeper)
+  int want_hstride = kPathHint;
   unsigned long long* d_bytes = nullptr;  // [0] match bytes, [1] group bytes
   ApiOut* d_api = nullptr;
   ApiOut api;
@@ -513,6 +518,25 @@ void reserve_window(e2_handle* h, u64 entries) {
   d.wcap = cap;
 }
 
+// Path log rings: grown (up to a bound) when an instance's live log passes
+// half the ring; entries that do not fit are simply not logged (their hit
+// stamps are undone by the parent-chain walk instead).
+constexpr u64 kPlogMin = 1ull << 16, kPlogMax = 1ull << 21;
+void reserve_plog(e2_handle* h) {
+  Dev& d = h->d;
+  if (!d.plog) {
+    d.pcap = kPlogMin;
+    d.plog = talloc<u32>(d.pcap * (u64)h->G);
+    return;
+  }
+  u64 live = 0;
+  for (int g = 0; g < h->G; ++g) live = std::max<u64>(live, h->hot.pl_tail[g] - h->hot.pl_head[g]);
+  if (live * 2 <= d.pcap || d.pcap >= kPlogMax) return;
+  const u64 cap = std::min<u64>(d.pcap * 4, kPlogMax);
+  ring_regrow(h, d.plog, d.pcap, cap, h->hot.pl_head, h->hot.pl_tail);
+  d.pcap = cap;
+}
+
 void reserve_fifo(e2_handle* h, u64 entries) {
   Dev& d = h->d;
   u64 cap = pow2_at_least(std::max<u64>(entries, 64));
@@ -569,6 +593,12 @@ void reserve_requests(e2_handle* h, i64 need) {
 }
 
 void reserve_batch(e2_handle* h, i64 B) {
+  if (h->want_hstride > h->hstride && h->bcap > 0) {
+    // paths got deeper than the hint stride in an earlier batch
+    dfree(h->b_path);
+    h->hstride = h->want_hstride;
+    h->b_path = talloc<u32>(h->bcap * h->hstride);
+  }
   if (B <= h->bcap) return;
   i64 cap = std::max<i64>(B, 256);
   dfree(h->b_S);
@@ -591,7 +621,7 @@ void reserve_batch(e2_handle* h, i64 B) {
   h->b_o = talloc<i64>(cap);
   h->b_dslot = talloc<u32>(cap);
   h->b_dm = talloc<u32>(cap);
-  h->b_path = talloc<u32>(cap * kPathHint);
+  h->b_path = talloc<u32>(cap * h->hstride);
   h->b_state = talloc<i32>(cap);
   h->b_A = talloc<u64>(cap);
   h->b_B = talloc<u64>(cap);
@@ -640,6 +670,7 @@ void reserve_for(e2_handle* h, i64 req, i64 toks) {
     maxf = std::max<u64>(maxf, h->hot.fifo_tail[g] - h->hot.fifo_head[g]);
   }
   reserve_window(h, maxw + (u64)req + 1);
+  reserve_plog(h);
   reserve_fifo(h, maxf + (u64)req + 1);
   reserve_inflight(h, (u64)h->hot.inflight_n + (u64)req + 1);
 }
@@ -675,6 +706,14 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
   }
 }
 
+// A K1 path reached `levels` >= the hint stride: grow it for later batches.
+void note_depth(e2_handle* h, u64 levels) {
+  if (levels < (u64)h->hstride) return;
+  int want = h->hstride;
+  while ((u64)want <= levels && want < kMaxHint) want *= 2;
+  h->want_hstride = std::max(h->want_hstride, want);
+}
+
 // K1 + leader rounds for requests [base, base+n) of the arena index.
 // Produces h->b_L[0..n).
 void launch_match(e2_handle* h, i64 base, i64 n) {
@@ -687,8 +726,10 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
     unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
     h->acc.launches[E2_K_MATCH]++;
     upload_dev(h);
+    dset(h->d_cnt + 2, 0, 4, h->stream);
     k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
-                                                             h->b_dm, h->b_path, h->d_bytes);
+                                                             h->b_dm, h->b_path, h->hstride, h->d_bytes,
+                                                             h->d_cnt + 2);
     CK(cudaGetLastError());
   }
   h->acc.match_requests += n;
@@ -712,9 +753,10 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
     k_group_resolve<<<tg, 256, 0, h->stream>>>(n, round, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
                                                h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_cnt, h->d_cnt + 1);
     CK(cudaGetLastError());
-    unsigned int cnt[2];
-    d2h(cnt, h->d_cnt, 8, h->stream);
+    unsigned int cnt[3];
+    d2h(cnt, h->d_cnt, 12, h->stream);
     ssync(h->stream);
+    note_depth(h, cnt[2]);
     if (cnt[1]) throw Fail(E2_ERR_ARG, "intra-batch grouping hash collision");
     if (cnt[0] == 0) break;
     dset(h->g_tk, 0, tsz * 8, h->stream);
@@ -733,11 +775,12 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   for (i64 w = 0; w < n; ++w) {
     const i64 r = base + w;
     g_dev_h = h->d;
-    MatchRes m = match_one(d.tok + h->r_off[r], h->r_len[r], h->b_path + w * kPathHint);
+    MatchRes m = match_one(d.tok + h->r_off[r], h->r_len[r], h->b_path + w * h->hstride, h->hstride);
     S[w] = m.S;
     ds[w] = m.div_slot;
     dm[w] = m.div_m;
     h->d_bytes[0] += (unsigned long long)m.bytes;
+    if (m.levels >= h->hstride) note_depth(h, (u64)m.levels);
   }
   h->acc.match_requests += n;
   // leader rounds with std::map grouping (same recursion as the device)
@@ -825,6 +868,7 @@ void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match) 
   a.op = op;
   a.out = h->d_api;
   a.hint = need_match ? h->b_path : nullptr;
+  a.hstride = h->hstride;
   push_hot(h);
   launch_serial(h, a);
   pull_hot(h);
@@ -1152,10 +1196,16 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
 #endif
     h->d.hot_g = talloc<Hot>(1);
     h->d_api = talloc<ApiOut>(1);
-    h->d_cnt = talloc<unsigned int>(2);
+    h->d_cnt = talloc<unsigned int>(4);
+    h->d.xp_slot = talloc<u32>(kXPath + 1);
+    h->d.xp_m = talloc<u32>(kXPath + 1);
+    h->d.xp_cm = talloc<u64>(kXPath + 1);
+    h->d.xp_la0 = talloc<u64>(kXPath + 1);
+    h->d.xp_flag = talloc<u32>(kXPath + 1);
     h->d_bytes = talloc<unsigned long long>(2);
     reserve_nodes(h, 1024);
     reserve_window(h, 1024);
+    reserve_plog(h);
     reserve_fifo(h, 64);
     reserve_inflight(h, 64);
     reserve_tokens(h, 1 << 16);
@@ -1180,8 +1230,9 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
 void e2_destroy(e2_handle* h) {
   if (!h) return;
   Dev& d = h->d;
-  void* ptrs[] = {d.rec, d.ct, d.win, d.comp, d.dir, d.pg_la, d.pg_id, d.pg_slot, d.free_pages, d.inf, d.fifo_req,
+  void* ptrs[] = {d.rec, d.ct, d.win, d.comp, d.plog, d.dir, d.pg_la, d.pg_id, d.pg_slot, d.free_pages, d.inf, d.fifo_req,
                   d.fifo_tail, d.req_tail, d.scr_slot, d.scr_val, d.scr_la, d.scr_id, d.vic_slot, d.vic_tok, d.hot_g,
+                  d.xp_slot, d.xp_m, d.xp_cm, d.xp_la0, d.xp_flag,
                   h->tok, h->r_off, h->r_len, h->b_S, h->b_L, h->b_cand, h->b_leader, h->b_o, h->b_dslot, h->b_dm,
                   h->b_path, h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api,
                   h->st_ids, h->st_out, h->st_offs, h->st_arr, h->st_dec, h->st_cost, h->st_rat};
@@ -1668,6 +1719,8 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     for (i64 b0 = 0; b0 < n; b0 += B) {
       const i64 nb = std::min<i64>(B, n - b0);
       launch_match(h, b0, nb);
+      a.hint = h->b_path;  // the hint stride may have grown
+      a.hstride = h->hstride;
       a.base = b0;
       a.n = nb;
       launch_serial(h, a);
@@ -1682,6 +1735,7 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
         }
         break;
       }
+      reserve_plog(h);
     }
     prof_flush(h);
     if (!device_ptrs) {

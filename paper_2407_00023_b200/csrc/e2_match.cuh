@@ -54,11 +54,12 @@ struct MatchRes {
   i64 S;         // matched length against the snapshot
   u32 div_slot;  // node where the walk stopped (kRoot if nothing matched)
   u32 div_m;     // tokens matched inside div_slot
+  i64 levels;    // nodes on the matched path
   i64 bytes;     // algorithmic bytes
 };
 
-// Warp-wide walk with token comparison; records up to kPathHint path slots.
-E2_D MatchRes match_one(const i32* seq, i64 n, u32* path) {
+// Warp-wide walk with token comparison; records up to nh path slots.
+E2_D MatchRes match_one(const i32* seq, i64 n, u32* path, int nh) {
   MatchRes r;
   r.S = 0;
   r.div_slot = kRoot;
@@ -75,7 +76,7 @@ E2_D MatchRes match_one(const i32* seq, i64 n, u32* path) {
     const i64 lim = min_(len, n - pos);
     // first token equal by construction of the child key
     const i64 m = 1 + warp_lcp(DEV.tok + off + 1, seq + pos + 1, lim - 1);
-    if (path && level < kPathHint && lane0()) path[level] = ch;
+    if (path && level < nh && lane0()) path[level] = ch;
     level++;
     pos += m;
     cur = ch;
@@ -83,9 +84,10 @@ E2_D MatchRes match_one(const i32* seq, i64 n, u32* path) {
     r.div_m = (u32)m;
     if (m < len) break;
   }
-  if (path)
-    for (int l = level + lane(); l < kPathHint; l += kWidth) path[l] = kNil;
+  // kNil-terminated (readers never look past the terminator)
+  if (path && level < nh && lane0()) path[level] = kNil;
   r.S = pos;
+  r.levels = level;
   // B_match = 4*min(|p|, matched+1) + 4*matched + 32*(depth+1)
   r.bytes = 4 * min_(n, pos + 1) + 4 * pos + 32 * (depth + 1);
   return r;

@@ -43,7 +43,7 @@ struct NodeRec {
 };
 static_assert(sizeof(NodeRec) == 64, "node header must stay 64 bytes");
 
-E2_HDX u32 rec_stride(int G) { return (u32)(((64 + 16 * G) + 127) / 128 * 128); }
+E2_HDX constexpr u32 rec_stride(int G) { return (u32)(((64 + 16 * G) + 127) / 128 * 128); }
 E2_HDX double* rla(NodeRec* r) { return (double*)((char*)r + 64); }
 E2_HDX i32* rhits(NodeRec* r, int G) { return (i32*)((char*)r + 64 + 8 * G); }
 E2_HDX i32* rccc(NodeRec* r, int G) { return (i32*)((char*)r + 64 + 12 * G); }
@@ -80,8 +80,8 @@ struct WinEnt {
   double t;
   i64 missed;
   i64 est;
-  u32 slot;
-  u32 pad;
+  u32 slot;  // tail slot of the committed prompt
+  u32 plen;  // levels of its path in the instance's path log (kNil: not logged)
 };
 
 struct CompEnt {
@@ -93,8 +93,10 @@ constexpr u64 kEmptyKey = ~0ull;
 constexpr u64 kTombKey = ~0ull - 1;
 constexpr i64 kNoInflight = INT64_MIN;
 constexpr int kPage = 32;   // LRU keys per page
-constexpr int kPathHint = 64;  // path slots K1 records per request
-constexpr int kMaxPath = 256;  // levels a request keeps in shared memory
+constexpr int kPathHint = 1024;  // initial K1 hint stride (path slots per request, kNil-terminated)
+constexpr int kMaxHint = 16384;  // largest hint stride the host grows to
+constexpr int kMaxPath = 1024;  // path levels a request keeps in shared memory
+constexpr u32 kXPath = 1u << 16;  // deeper levels: global overflow (DEV.xp_*)
 
 // Error codes mirrored from e2sched.h.
 constexpr i32 kErrConfig = 1;
@@ -158,6 +160,7 @@ struct Hot {
   i64 wc_output_sum[kMaxG];
   u32 dir_head[kMaxG], dir_n[kMaxG];
   u64 fifo_head[kMaxG], fifo_tail[kMaxG];
+  u64 pl_head[kMaxG], pl_tail[kMaxG];  // path-log ring positions
   u64 next_id;
   i64 node_count;
   u32 slots_used;
@@ -189,6 +192,10 @@ struct Dev {
   u64 wcap;  // power of two per instance
   WinEnt* win;
   CompEnt* comp;
+  // path log: per instance ring of the slots of each window entry's root
+  // path (top-down), so expiring hit stamps are undone level-parallel
+  u64 pcap;  // power of two per instance
+  u32* plog;
   // LRU
   u32 dcap;  // directory ring per instance (power of two)
   u32 page_cap;
@@ -214,6 +221,12 @@ struct Dev {
   u64* scr_id;
   u32* vic_slot;
   i64* vic_tok;
+  // path levels >= kMaxPath of the request being processed
+  u32* xp_slot;
+  u32* xp_m;
+  u64* xp_cm;
+  u64* xp_la0;
+  u32* xp_flag;
   Hot* hot_g;
 };
 

@@ -66,9 +66,26 @@ E2_HD NodeRec* nentry(u32 w) { return (NodeRec*)(NC.data + (u64)w * DEV.rs); }
 // record the serial pass touches is modified anyway), so no dirty tracking.
 E2_HD void ndirty(const NodeRec*) {}
 
-// warp-wide copy of one record (rs bytes, 8-byte words)
+// warp-wide copy of one record (rs bytes, 8-byte words; at most
+// rec_stride(kMaxG)/8 = 144 words): every load is issued before the first
+// store, so a miss costs one memory latency, not one per 32 words.
 E2_D void rcopy(u64* dst, const u64* src, u32 words) {
-  for (u32 j = (u32)lane(); j < words; j += kWidth) dst[j] = src[j];
+#if E2_DEVICE_BUILD
+  constexpr int kPer = (rec_stride(kMaxG) / 8 + 31) / 32;
+  u64 v[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const u32 j = (u32)lane() + 32u * k;
+    if (j < words) v[k] = src[j];
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const u32 j = (u32)lane() + 32u * k;
+    if (j < words) dst[j] = v[k];
+  }
+#else
+  for (u32 j = 0; j < words; ++j) dst[j] = src[j];
+#endif
 }
 
 // warp-wide: pick the way to (re)use in s's set; write back its record.
