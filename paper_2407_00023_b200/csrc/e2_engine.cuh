@@ -22,6 +22,7 @@ struct Scr {
   i32 cinf[kMaxG + 1];
   double cL[kMaxG + 1], cM[kMaxG + 1], cP[kMaxG + 1];
   i32 n_costs;
+  i32 loads_ok;  // loads[] hold load_ms at this request's `now` (update_redirects ran)
   i32 npath;  // levels recorded by walk_par (-1: path too deep, sequential fallback)
   // the request's root path, top-down (walk_par / commit)
   u32 pslot[kMaxPath + 1];
@@ -316,9 +317,11 @@ struct CostOut {
   bool inf;
 };
 
-E2_HD CostOut cost_for(int g, i64 missed, double now) {
+E2_HD CostOut cost_for(int g, i64 missed, double now, const Scr* s = nullptr) {
   CostOut o;
-  o.L = win_load(g, now);
+  // update_redirects already computed load_ms(g, now) this request; nothing
+  // touches the windows between it and the cost evaluation
+  o.L = (s && s->loads_ok) ? s->loads[g] : win_load(g, now);
   o.P = prefill_time(DEV.cfg, missed);
   o.M = 0.0;
   o.inf = false;
@@ -483,20 +486,22 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
       const u32 nilm = ballot(c == kNil);
       in = k < (nilm ? ffs32(nilm) : 32);
       u32 par = kNil;
-      i32 ft = 0;
-      i64 len = 0;
+      i64 len = 0, pk = 0;
       u64 cm = 0;
       if (in) {
         const NodeRec* r = npeek(c);
         par = r->parent;
-        ft = r->first_tok;
         len = r->edge_len;
         cm = r->cmask;
+        pk = r->depth;
       }
-      const i64 pk = pos + warp_incl_sum(len) - len;
+      // A hint is K1's node for this very prompt.  If its parent is still
+      // the previous level's node, no split has cut the chain since K1, so
+      // the edge still starts at its stored depth and its first token is
+      // the prompt's (K1 followed the child table with it): no token load.
       u32 prev = __shfl_up_sync(0xffffffffu, c, 1);
       if (k == 0) prev = cur;
-      const bool ok = in && par == prev && len > 0 && pk < L && seq[pk] == ft;
+      const bool ok = in && par == prev && len > 0 && pk < L;
       const u32 okm = ballot(ok);
       const int nvalid = (okm == 0xffffffffu) ? 32 : ffs32(~okm);
       const u32 lastm = ballot(ok && pk + len >= L) & (nvalid == 32 ? 0xffffffffu : ((1u << nvalid) - 1));
@@ -533,10 +538,18 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
       if (c != kNil) {
         r = nget(c);
         if (r->parent == cur && r->first_tok == t && r->edge_len > 0) ch = c;
+#if !E2_DEVICE_BUILD
+        else if (r->parent != cur) PHASE_COUNT(6);
+        else PHASE_COUNT(7);
+#endif
       }
+#if !E2_DEVICE_BUILD
+      else PHASE_COUNT(8);
+#endif
     }
     if (ch == kNil) {
       fast = false;
+      PHASE_COUNT(12);
       ch = child_lookup(cur, t);
       if (ch == kNil) {
         w.ok = false;
@@ -695,31 +708,74 @@ E2_DNI u32 ensure_path(i64 seq_off, i64 n, i64 L, const Walk& w) {
 // ---------------------------------------------------------------------------
 E2_DNI void update_redirects(Scr* s, double now) {
   const int G = DEV.cfg.G;
+  const double th = DEV.cfg.th_bal;
   for (int g = lane(); g < G; g += kWidth) s->loads[g] = win_load(g, now);
   wsync();
+  // expiry: each redirect's check reads only the loads (lane per source)
+  for (int src = lane(); src < G; src += kWidth) {
+    const int dst = HOT.redirect[src];
+    if (dst >= 0 && s->loads[src] <= dmul(th, s->loads[dst])) HOT.redirect[src] = -1;
+  }
+  // hi / lo: first index of the max / min (strict > / < scans from 0)
+  int hi = 0, lo = 0;
+#if E2_DEVICE_BUILD
+  {
+    int ih = -1, il = -1;
+    double vh = 0, vl = 0;
+    for (int g = lane(); g < G; g += kWidth) {
+      const double v = s->loads[g];
+      if (ih < 0 || v > vh) { vh = v; ih = g; }
+      if (il < 0 || v < vl) { vl = v; il = g; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double wh = __shfl_xor_sync(0xffffffffu, vh, o), wl = __shfl_xor_sync(0xffffffffu, vl, o);
+      const int jh = __shfl_xor_sync(0xffffffffu, ih, o), jl = __shfl_xor_sync(0xffffffffu, il, o);
+      if (jh >= 0 && (ih < 0 || wh > vh || (wh == vh && jh < ih))) { vh = wh; ih = jh; }
+      if (jl >= 0 && (il < 0 || wl < vl || (wl == vl && jl < il))) { vl = wl; il = jl; }
+    }
+    hi = ih;
+    lo = il;
+  }
+#else
+  for (int g = 1; g < G; ++g) {
+    if (s->loads[g] > s->loads[hi]) hi = g;
+    if (s->loads[g] < s->loads[lo]) lo = g;
+  }
+#endif
+  wsync();
   if (lane0()) {
-    const double th = DEV.cfg.th_bal;
-    for (int src = 0; src < G; ++src) {
-      const int dst = HOT.redirect[src];
-      if (dst >= 0 && s->loads[src] <= dmul(th, s->loads[dst])) HOT.redirect[src] = -1;
-    }
-    int hi = 0, lo = 0;
-    for (int g = 1; g < G; ++g) {
-      if (s->loads[g] > s->loads[hi]) hi = g;
-      if (s->loads[g] < s->loads[lo]) lo = g;
-    }
     if (!(hi == lo || !(s->loads[hi] > dmul(th, s->loads[lo])))) {
       if (HOT.redirect[hi] != lo) {
         HOT.redirect[hi] = lo;
         HOT.stats[kStInstalls]++;
       }
     }
+    s->loads_ok = 1;
   }
   wsync();
 }
 
-// pick_min_cost (global_scheduler.cpp:54-74) over s->c*[0, n).
+// pick_min_cost (global_scheduler.cpp:54-74) over s->c*[0, n): the first
+// index with the minimum total among the feasible candidates, else among all.
+// Device: one lane per candidate and a (total, index) warp reduction.
 E2_HD int pick_min(const Scr* s, int n) {
+#if E2_DEVICE_BUILD
+  int bf = -1, ba = -1;  // best feasible / best overall candidate index
+  double tf = 0, ta = 0;
+  for (int i = lane(); i < n; i += kWidth) {
+    const double t = dadd(dadd(s->cL[i], s->cM[i]), s->cP[i]);
+    if (!s->cinf[i] && (bf < 0 || t < tf)) { tf = t; bf = i; }
+    if (ba < 0 || t < ta) { ta = t; ba = i; }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double uf = __shfl_xor_sync(0xffffffffu, tf, o), ua = __shfl_xor_sync(0xffffffffu, ta, o);
+    const int jf = __shfl_xor_sync(0xffffffffu, bf, o), ja = __shfl_xor_sync(0xffffffffu, ba, o);
+    if (jf >= 0 && (bf < 0 || uf < tf || (uf == tf && jf < bf))) { tf = uf; bf = jf; }
+    if (ja >= 0 && (ba < 0 || ua < ta || (ua == ta && ja < ba))) { ta = ua; ba = ja; }
+  }
+  const int b = bf >= 0 ? bf : ba;
+  return b >= 0 ? s->cgpu[b] : -1;
+#else
   int best = -1;
   double bt = 0;
   for (int i = 0; i < n; ++i) {
@@ -739,6 +795,7 @@ E2_HD int pick_min(const Scr* s, int n) {
     }
   }
   return best;
+#endif
 }
 
 struct Dec {
@@ -789,8 +846,10 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
   }
   if (lane0()) HOT.stats[kStTreeReads]++;
   wsync();
+  PHASE_MARK(1);
   w = walk_par(seq, L, hint, nhint, s);
   if (!w.ok && s->npath < 0) w = walk_known(seq, L, hint, nhint, s->ext);
+  PHASE_MARK(6);
   if (!w.ok) {
     if (lane0()) set_err(kErrSim, kWhyWalk);
     wsync();
@@ -827,11 +886,13 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
       if (s->ext[g] == best) cand |= (1ull << g);
     }
 #endif
+    PHASE_MARK(1);
     cost_prepare_set(s, cand, n, now);
+    PHASE_MARK(7);
     for (int g = lane(); g < G; g += kWidth) {
       if ((cand >> g) & 1ull) {
         const int idx = popc64(cand & ((1ull << g) - 1));
-        put_cost(s, idx, g, cost_for(g, n - s->ext[g], now));
+        put_cost(s, idx, g, cost_for(g, n - s->ext[g], now, s));
       }
     }
     wsync();
@@ -844,7 +905,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
         if (s->cgpu[i] == t) ti = i;
       if (ti < 0) {
         cost_prepare(t, n - s->ext[t], now);
-        if (lane0()) put_cost(s, nc, t, cost_for(t, n - s->ext[t], now));
+        if (lane0()) put_cost(s, nc, t, cost_for(t, n - s->ext[t], now, s));
         wsync();
         ti = nc;
         nc++;
@@ -858,6 +919,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
     if (lane0()) s->n_costs = nc;
     wsync();
     r.gpu = gpu;
+    PHASE_MARK(8);
   } else {
     r.has_ratios = 1;
     for (int g = lane(); g < G; g += kWidth) {
@@ -879,7 +941,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
     } else {
       r.branch = 1;
       cost_prepare_set(s, G == 64 ? ~0ull : ((1ull << G) - 1), n, now);
-      for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(g, n - s->ext[g], now));
+      for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(g, n - s->ext[g], now, s));
       wsync();
       if (lane0()) s->n_costs = G;
       wsync();
@@ -1005,7 +1067,9 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
     wsync();
     return kNil;
   }
+  PHASE_MARK(2);
   const u32 tail = ensure_path(seq_off, n, L, w);
+  PHASE_MARK(9);
   if (tail == kNil || HOT.err) return kNil;
   const int g = r.gpu;
   u64 root_id;
@@ -1031,6 +1095,7 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
   u32 plen = kNil;
   if (D >= 0) {
     root_id = path_update_par(s_path, D, g, now, mark);
+    PHASE_MARK(10);
     plen = plog_append(s_path, D, g);
   } else {
     root_id = path_update(tail, g, now, mark);
@@ -1234,15 +1299,19 @@ E2_DNI void evict_lru(int g, i64 over) {
     DEV.scr_val[(u64)DEV.cfg.G * DEV.scap] = nv;  // count, in the spare scratch word
   }
   wsync();
+  PHASE_MARK(11);
   const u32 nv = (u32)DEV.scr_val[(u64)DEV.cfg.G * DEV.scap];
   for (u32 i = 0; i < nv && !HOT.err; ++i) {
     const u32 v = DEV.vic_slot[i];
     const i64 tok = DEV.vic_tok[i];
     const i64 len = nget(v)->edge_len;
-    if (tok < len)
+    if (tok < len) {
+      PHASE_COUNT(13);
       evict_tail(v, tok, g);
-    else
+    } else {
+      PHASE_COUNT(14);
       clear_cached(v, g);
+    }
   }
 }
 

@@ -213,6 +213,8 @@ E2_D void subtree_apply(u32 root, int g, double now, bool mark) {
 
 E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, int nh, ApiOut* out) {
   const int G = DEV.cfg.G;
+  if (lane0()) s->loads_ok = 0;
+  wsync();
   const i32* seq = DEV.tok + op.off;
   switch (op.kind) {
     case OP_SCHEDULE:
@@ -335,18 +337,8 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, int nh, ApiOut* out)
   }
 }
 
-#if defined(E2_PHASES) && E2_DEVICE_BUILD
-#define PHASE_T0() u64 _pt = clock64()
-#define PHASE(i)                                      \
-  do {                                                \
-    const u64 _pn = clock64();                        \
-    if (lane0()) HOT.phase_cycles[i] += _pn - _pt;    \
-    _pt = _pn;                                        \
-  } while (0)
-#else
-#define PHASE_T0()
-#define PHASE(i)
-#endif
+#define PHASE_T0() PHASE_MARK(15)
+#define PHASE(i) PHASE_MARK(i)
 
 // One request of the generalised criterion-7 loop (e2sched.h, e2_replay).
 E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
@@ -356,7 +348,10 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
   const i32* seq = DEV.tok + off;
   PHASE_T0();
   const double now = max_(HOT.drv_now, a.arr[r]);
-  if (lane0()) HOT.drv_now = now;
+  if (lane0()) {
+    HOT.drv_now = now;
+    s->loads_ok = 0;
+  }
   wsync();
   if (DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, now);
   PHASE(0);

@@ -122,6 +122,7 @@ void grow(T*& p, size_t keep, size_t n, Stream s) {
 namespace {
 
 constexpr int kMatchWarpsPerBlock = 8;
+constexpr i64 kFirstBatch = 256;  // replay batch-size ramp start
 
 #if E2_DEVICE_BUILD
 __global__ void __launch_bounds__(32, 1) k_serial(SerialArgs a, u32 nsets) {
@@ -156,22 +157,37 @@ __global__ void __launch_bounds__(32, 1) k_serial(SerialArgs a, u32 nsets) {
   }
 }
 
-__global__ void __launch_bounds__(kMatchWarpsPerBlock * 32) k_match(i64 n, i64 base, const i64* off,
-                                                                     const i64* len, i64* S, u32* dslot, u32* dm,
-                                                                     u32* path, int hstride,
-                                                                     unsigned long long* bytes,
-                                                                     unsigned int* max_levels) {
-  const i64 w = (i64)blockIdx.x * kMatchWarpsPerBlock + (threadIdx.x >> 5);
-  if (w >= n) return;
-  const i64 r = base + w;
-  MatchRes m = match_one(g_dev.tok + off[r], len[r], path + w * hstride, hstride);
-  if (lane0()) {
-    S[w] = m.S;
-    dslot[w] = m.div_slot;
-    dm[w] = m.div_m;
-    atomicAdd(bytes, (unsigned long long)m.bytes);
-    if (m.levels >= hstride) atomicMax(max_levels, (unsigned int)min_<i64>(m.levels, 0x7fffffff));
+// Persistent: kMatchBlocksPerSM blocks per SM; each warp takes requests from
+// a global counter (fetched one ahead, so the atomic's latency hides behind
+// the current match) until the batch is drained.
+constexpr int kMatchBlocksPerSM = 4;
+__global__ void __launch_bounds__(kMatchWarpsPerBlock * 32, kMatchBlocksPerSM)
+    k_match(i64 n, i64 base, const i64* off, const i64* len, i64* S, u32* dslot, u32* dm, u32* path, int hstride,
+            unsigned long long* bytes, unsigned int* max_levels, unsigned int* next) {
+  unsigned long long acc = 0;
+  unsigned int w = 0;
+  if (lane0()) w = atomicAdd(next, 1u);
+  w = shfl(w, 0);
+  while ((i64)w < n) {
+    unsigned int wn = 0;
+    if (lane0()) wn = atomicAdd(next, 1u);
+    const MatchRes m = match_one(g_dev.tok + off[base + w], len[base + w], path + (i64)w * hstride, hstride);
+    if (lane0()) {
+      S[w] = m.S;
+      dslot[w] = m.div_slot;
+      dm[w] = m.div_m;
+      if (m.levels >= hstride) atomicMax(max_levels, (unsigned int)min_<i64>(m.levels, 0x7fffffff));
+    }
+    acc += (unsigned long long)m.bytes;
+    w = shfl(wn, 0);
   }
+  // algorithmic-byte counter: one global atomic per block
+  __shared__ unsigned long long blk_bytes;
+  if (threadIdx.x == 0) blk_bytes = 0;
+  __syncthreads();
+  if (lane0()) atomicAdd(&blk_bytes, acc);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(bytes, blk_bytes);
 }
 
 __device__ __forceinline__ void gtab_insert(u64* tk, u32* tv, u64 mask, u64 key, u32 i) {
@@ -304,6 +320,7 @@ struct e2_handle {
   u64* g_tk = nullptr;
   u32* g_tv = nullptr;
   u64 g_mask = 0;
+  int n_sm = 148;
   unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions, [2] deepest K1 path beyond the hint stride
   int hstride = kPathHint;             // K1 path hints per request (grown when paths get deeper)
   int want_hstride = kPathHint;
@@ -722,14 +739,15 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   Dev& d = h->d;
 #if E2_DEVICE_BUILD
   {
-    Timed t(h, E2_K_MATCH);
-    unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
+    const i64 blocks = (n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock;
+    const unsigned grid = (unsigned)std::min<i64>(blocks, (i64)h->n_sm * kMatchBlocksPerSM);
     h->acc.launches[E2_K_MATCH]++;
     upload_dev(h);
-    dset(h->d_cnt + 2, 0, 4, h->stream);
+    dset(h->d_cnt + 2, 0, 8, h->stream);  // [2] deepest path, [3] work counter
+    Timed t(h, E2_K_MATCH);  // the kernel alone (roofline denominator)
     k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
                                                              h->b_dm, h->b_path, h->hstride, h->d_bytes,
-                                                             h->d_cnt + 2);
+                                                             h->d_cnt + 2, h->d_cnt + 3);
     CK(cudaGetLastError());
   }
   h->acc.match_requests += n;
@@ -1181,7 +1199,11 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     {
       // node cache: as many 4-way sets as fit in ~150 KB of shared memory
       u32 ne = 1;
+#if !defined(E2_NOCACHE)
       while ((u64)(ne * 2) * (h->d.rs + 12) <= 150u * 1024 && ne * 2 <= 1024) ne *= 2;
+#else
+      ne = kWays;
+#endif
       h->nsets = std::max<u32>(ne / kWays, 1);
       const u32 e = h->nsets * kWays;
       h->serial_smem = ((3 * e * 4 + 15) / 16) * 16 + (size_t)e * h->d.rs;
@@ -1190,6 +1212,11 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     CK(cudaFuncSetAttribute(k_serial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->serial_smem));
 #endif
 #if E2_DEVICE_BUILD
+    {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream_handle = h->stream;
     h->own_stream = true;
@@ -1716,8 +1743,12 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     i64 done = 0;
     std::string fail;
     int fail_code = 0;
-    for (i64 b0 = 0; b0 < n; b0 += B) {
-      const i64 nb = std::min<i64>(B, n - b0);
+    // Batch sizes ramp up geometrically from kFirstBatch: a batch is matched
+    // against the tree at its start, so early batches (a cold tree) would
+    // leave most requests without K1 path hints.
+    i64 cur_b = std::min<i64>(B, kFirstBatch);
+    for (i64 b0 = 0; b0 < n; b0 += cur_b, cur_b = std::min<i64>(B, cur_b * 2)) {
+      const i64 nb = std::min<i64>(cur_b, n - b0);
       launch_match(h, b0, nb);
       a.hint = h->b_path;  // the hint stride may have grown
       a.hstride = h->hstride;
@@ -1801,7 +1832,7 @@ int e2_profile_reset(e2_handle* h, int32_t enable_timing) {
 extern "C" int e2_debug_phases(e2_handle* h, uint64_t* out) {
   return guard(h, [&] {
     pull_hot(h);
-    for (int i = 0; i < 8; ++i) out[i] = h->hot.phase_cycles[i];
+    for (int i = 0; i < 16; ++i) out[i] = h->hot.phase_cycles[i];
   });
 }
 #endif

@@ -22,27 +22,92 @@
 
 namespace e2 {
 
-// First index in [0, lim) where a and b differ, or lim.  Warp-wide.
-E2_D i64 warp_lcp(const i32* a, const i32* b, i64 lim) {
 #if E2_DEVICE_BUILD
+// Tokens R..R+3 of the 8-token window (x, y): realigns the tree side's
+// 16-byte quads to the prompt's phase (R is the phase difference).
+template <int R>
+E2_D int4 funnel4(const int4& x, const int4& y) {
+  if (R == 0) return x;
+  if (R == 1) return make_int4(x.y, x.z, x.w, y.x);
+  if (R == 2) return make_int4(x.z, x.w, y.x, y.y);
+  return make_int4(x.w, y.x, y.y, y.z);
+}
+
+// Valid-token mask of a quad whose element 0 is token t0, tokens [0, lim).
+E2_D u32 quad_mask(i64 t0, i64 lim) {
+  const i64 hi = lim - t0;
+  u32 vm = hi >= 4 ? 0xfu : hi <= 0 ? 0u : ((1u << (u32)hi) - 1u);
+  if (t0 < 0) vm &= ~((1u << (u32)(-t0)) - 1u);
+  return vm;
+}
+
+constexpr int kLcpU = 2;  // quads per lane per side in flight per step (kLcpU*128 tokens)
+
+// b-frame quad q (element k = token 4q+k-sb); a-frame index t+sa = 4(q+dq)+k+R.
+template <int R>
+E2_D i64 warp_lcp_phase(const int4* A4, const int4* B4, int sb, int dq, i64 lim) {
   const int l = lane();
-  for (i64 base = 0; base < lim; base += 4 * kWidth) {
-    i32 av[4], bv[4];
-    bool in[4];
+  const i64 qb_end = (lim + sb + 3) >> 2;
+  const i64 qa_end = (lim + sb + dq * 4 + R + 3) >> 2;  // (lim + sa + 3) >> 2
+  for (i64 q0 = 0; q0 < qb_end; q0 += kLcpU * 32) {
+    int4 bv[kLcpU], xv[kLcpU], zv[kLcpU];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      i64 i = base + l + 32 * k;
-      in[k] = i < lim;
-      av[k] = in[k] ? __ldg(a + i) : 0;
-      bv[k] = in[k] ? __ldcs(b + i) : 0;  // prompt side streams (evict-first in L2)
+    for (int u = 0; u < kLcpU; ++u) {
+      const i64 q = q0 + l + 32 * u;
+      const i64 qa = q + dq;
+      bv[u] = q < qb_end ? __ldcs(B4 + q) : make_int4(0, 0, 0, 0);
+      xv[u] = (qa >= 0 && qa < qa_end) ? __ldg(A4 + qa) : make_int4(0, 0, 0, 0);
+      if (R != 0) zv[u] = (l == 31 && qa + 1 < qa_end) ? __ldg(A4 + qa + 1) : make_int4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      u32 m = ballot(in[k] && av[k] != bv[k]);
-      if (m) return base + 32 * k + ffs32(m);
+    for (int u = 0; u < kLcpU; ++u) {
+      int4 av = xv[u];
+      if (R != 0) {
+        int4 yv;
+        yv.x = __shfl_down_sync(0xffffffffu, xv[u].x, 1);
+        yv.y = __shfl_down_sync(0xffffffffu, xv[u].y, 1);
+        yv.z = __shfl_down_sync(0xffffffffu, xv[u].z, 1);
+        yv.w = __shfl_down_sync(0xffffffffu, xv[u].w, 1);
+        if (l == 31) yv = zv[u];
+        av = funnel4<R>(xv[u], yv);
+      }
+      const i64 t0 = 4 * (q0 + l + 32 * u) - sb;  // token index of element 0
+      u32 mm = (av.x != bv[u].x ? 1u : 0u) | (av.y != bv[u].y ? 2u : 0u) | (av.z != bv[u].z ? 4u : 0u) |
+               (av.w != bv[u].w ? 8u : 0u);
+      mm &= quad_mask(t0, lim);
+      const u32 wm = ballot(mm != 0);
+      if (wm) {
+        const int f = ffs32(wm);
+        const u32 fm = shfl(mm, f);
+        return 4 * (q0 + f + 32 * u) - sb + ffs32(fm);
+      }
     }
   }
   return lim;
+}
+#endif
+
+// First index in [0, lim) where a and b differ, or lim.  Warp-wide.
+// Device: 128-bit loads on both sides.  The prompt side b streams as aligned
+// int4 quads (evict-first in L2: read once); the tree side a (edge tokens,
+// shared by many prompts: L1/L2-resident) is read as aligned quads too and
+// realigned to b's phase from the lane's quad and its neighbour's (shfl);
+// the phase difference is warp-uniform, so each phase has its own loop.
+E2_D i64 warp_lcp(const i32* a, const i32* b, i64 lim) {
+#if E2_DEVICE_BUILD
+  if (lim <= 0) return 0;
+  const int sb = (int)(((unsigned long long)b >> 2) & 3);
+  const int sa = (int)(((unsigned long long)a >> 2) & 3);
+  const int4* B4 = (const int4*)(b - sb);
+  const int4* A4 = (const int4*)(a - sa);
+  const int dd = sa - sb;
+  const int dq = dd < 0 ? -1 : 0;
+  switch (dd - 4 * dq) {
+    case 0: return warp_lcp_phase<0>(A4, B4, sb, dq, lim);
+    case 1: return warp_lcp_phase<1>(A4, B4, sb, dq, lim);
+    case 2: return warp_lcp_phase<2>(A4, B4, sb, dq, lim);
+    default: return warp_lcp_phase<3>(A4, B4, sb, dq, lim);
+  }
 #else
   i64 i = 0;
   while (i < lim && a[i] == b[i]) ++i;

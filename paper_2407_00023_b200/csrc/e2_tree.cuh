@@ -53,6 +53,31 @@ inline NCache g_nc_h;
 
 E2_HD NodeRec* grec(u32 s) { return (NodeRec*)(DEV.rec + (u64)s * DEV.rs); }
 
+// E2_PHASES (dev-only instrumented builds): cycles since the previous mark
+// are added to phase_cycles[i].  Compiled out of the product.
+#if defined(E2_PHASES) && E2_DEVICE_BUILD
+#define PHASE_MARK(i)                                          \
+  do {                                                         \
+    __syncwarp();                                              \
+    const u64 _pn = clock64();                                 \
+    if (lane0()) {                                             \
+      HOT.phase_cycles[i] += _pn - HOT.phase_last;             \
+      HOT.phase_last = _pn;                                    \
+    }                                                          \
+    __syncwarp();                                              \
+  } while (0)
+#else
+#define PHASE_MARK(i)
+#endif
+#if defined(E2_PHASES)
+#define PHASE_COUNT(i)                                         \
+  do {                                                         \
+    if (lane0()) HOT.phase_cycles[i] += 1;                     \
+  } while (0)
+#else
+#define PHASE_COUNT(i)
+#endif
+
 E2_HD void set_err(i32 code, i32 why) {
   if (HOT.err == 0) {
     HOT.err = code;
@@ -66,6 +91,20 @@ E2_HD NodeRec* nentry(u32 w) { return (NodeRec*)(NC.data + (u64)w * DEV.rs); }
 // record the serial pass touches is modified anyway), so no dirty tracking.
 E2_HD void ndirty(const NodeRec*) {}
 
+#if defined(E2_NOCACHE) && E2_DEVICE_BUILD
+// Variant without the shared-memory node cache: records are read and written
+// in place in HBM, through L1/L2.
+E2_D NodeRec* nget(u32 s) { return grec(s); }
+E2_DNI NodeRec* nnew(u32 s) {
+  u64* dst = (u64*)grec(s);
+  for (u32 j = (u32)lane(); j < DEV.rs / 8; j += kWidth) dst[j] = 0;
+  wsync();
+  return grec(s);
+}
+E2_HD const NodeRec* npeek(u32 s) { return grec(s); }
+E2_HD NodeRec* npoke(u32 s) { return grec(s); }
+E2_D void nflush() {}
+#else
 // warp-wide copy of one record (rs bytes, 8-byte words; at most
 // rec_stride(kMaxG)/8 = 144 words): every load is issued before the first
 // store, so a miss costs one memory latency, not one per 32 words.
@@ -174,6 +213,8 @@ E2_D void nflush() {
   }
   wsync();
 }
+
+#endif
 
 // ---------------------------------------------------------------------------
 // Child table: open addressing, linear probing, key = parent<<32 | token.
