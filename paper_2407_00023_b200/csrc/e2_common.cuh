@@ -47,6 +47,8 @@ E2_D u32 ballot(bool p) { return __ballot_sync(0xffffffffu, p); }
 E2_D bool any(bool p) { return __any_sync(0xffffffffu, p); }
 template <typename T>
 E2_D T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+template <typename T>
+E2_D T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 E2_D int ffs32(u32 m) { return __ffs((int)m) - 1; }
 E2_D int popc32(u32 m) { return __popc(m); }
 E2_D int popc64(u64 m) { return __popcll(m); }
@@ -66,6 +68,8 @@ inline u32 ballot(bool p) { return p ? 1u : 0u; }
 inline bool any(bool p) { return p; }
 template <typename T>
 inline T shfl(T v, int) { return v; }
+template <typename T>
+inline T shfl_up1(T v) { return v; }
 inline int ffs32(u32 m) { return m ? __builtin_ctz(m) : -1; }
 inline int popc32(u32 m) { return __builtin_popcount(m); }
 inline int popc64(u64 m) { return __builtin_popcountll(m); }

@@ -457,7 +457,10 @@ E2_D i64 warp_sum(i64 v) {
 // s->pslot/pm/pcm and derives the per-gpu extents and cached_len from it
 // (prefix_tree.cpp:79-114).  s->npath = -1 when the path exceeds kMaxPath:
 // the caller then uses the sequential walk.
-E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) {
+// hS: K1's snapshot match length.  A hinted slot is on this prompt's path
+// only while its (current) start lies below hS: the last hint may be a node
+// K1 matched only partially, whose slot now holds the part past hS.
+E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, i64 hS) {
   Walk w;
   w.last = kRoot;
   w.last_m = 0;
@@ -465,11 +468,12 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
   w.present = 0;
   w.ok = true;
   const int G = DEV.cfg.G;
-  int np = 0;
+  int np = 0, hi = 0;  // path levels recorded, hints consumed
   i64 pos = 0;
   u32 cur = kRoot;
   bool fast = hint != nullptr;
   bool done = false;
+  constexpr u32 kFull = kWidth == 32 ? 0xffffffffu : 1u;
   while (pos < L && !done) {
     if (np >= kPathLevels) {
       if (lane0()) s->npath = -1;
@@ -477,14 +481,13 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
       w.ok = false;
       return w;
     }
-#if E2_DEVICE_BUILD
-    if (fast && np < nhint) {
-      const int k = lane(), lvl = np + k;
-      bool in = lvl < nhint && lvl < kPathLevels;
-      const u32 c = in ? hint[lvl] : kNil;
+    if (fast && hi < nhint) {
+      // kWidth hinted levels at once, one per lane
+      const int k = lane(), lvl = hi + k;
+      const u32 c = lvl < nhint ? hint[lvl] : kNil;
       // K1 terminates the hint list with kNil; nothing after it is read
       const u32 nilm = ballot(c == kNil);
-      in = k < (nilm ? ffs32(nilm) : 32);
+      const bool in = k < (nilm ? ffs32(nilm) : kWidth) && np + k < kPathLevels;
       u32 par = kNil;
       i64 len = 0, pk = 0;
       u64 cm = 0;
@@ -499,64 +502,106 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s) 
       // the previous level's node, no split has cut the chain since K1, so
       // the edge still starts at its stored depth and its first token is
       // the prompt's (K1 followed the child table with it): no token load.
-      u32 prev = __shfl_up_sync(0xffffffffu, c, 1);
+      u32 prev = shfl_up1(c);
       if (k == 0) prev = cur;
-      const bool ok = in && par == prev && len > 0 && pk < L;
+      const bool ok = in && par == prev && len > 0 && pk < hS;
       const u32 okm = ballot(ok);
-      const int nvalid = (okm == 0xffffffffu) ? 32 : ffs32(~okm);
+      const int nvalid = (okm == kFull) ? kWidth : ffs32(~okm);
       const u32 lastm = ballot(ok && pk + len >= L) & (nvalid == 32 ? 0xffffffffu : ((1u << nvalid) - 1));
       const int used = lastm ? ffs32(lastm) + 1 : nvalid;
-      if (used == 0) {
+      if (used > 0) {
+        const i64 m = min_(len, L - pk);
+        if (k < used) {
+          PSLOT(s, np + k) = c;
+          PM(s, np + k) = (u32)m;
+          PCM(s, np + k) = cm;
+        }
+        const u32 lc = shfl(c, used - 1);
+        const i64 lm = shfl(m, used - 1), lp = shfl(pk, used - 1), ll = shfl(len, used - 1);
+        wsync();
+        np += used;
+        hi += used;
+        pos = lp + lm;
+        cur = lc;
+        w.last = lc;
+        w.last_m = lm;
+        if (lastm) done = true;  // reached L (or the match ends inside this edge)
+        if (lm < ll) done = true;
+        continue;
+      }
+      // The next hint does not hang off `cur`.  Splits since K1 keep every
+      // hinted slot on the path (the slot keeps the suffix, whose end is
+      // unchanged) and insert the prefix halves above it: climb from the
+      // hint's parent to `cur` and take the inserted nodes as levels.
+      const bool in0 = shfl((int)in, 0) != 0;
+      const u32 p0 = shfl(par, 0);
+      const i64 l0 = shfl(len, 0);
+      if (!in0 || l0 == 0 || p0 == cur || p0 == kNil) {
         fast = false;
         continue;
       }
-      const i64 m = min_(len, L - pk);
-      if (k < used) {
-        PSLOT(s, np + k) = c;
-        PM(s, np + k) = (u32)m;
-        PCM(s, np + k) = cm;
+      int nc = 0;
+      u32 x = p0;
+      while (x != cur && x != kRoot && x != kNil && nc < 32 && np + nc < kPathLevels) {
+        if (lane0()) PSLOT(s, np + nc) = x;
+        nc++;
+        x = npeek(x)->parent;
       }
-      const u32 lc = shfl(c, used - 1);
-      const i64 lm = shfl(m, used - 1), lp = shfl(pk, used - 1), ll = shfl(len, used - 1);
       wsync();
-      np += used;
+      if (x != cur || nc == 0) {
+        fast = false;
+        continue;
+      }
+      // take up to kWidth levels from the top of the chain (the rest, if
+      // any, is climbed again on the next pass)
+      const int ntop = nc;
+      nc = min_(nc, kWidth);
+      u32 v = kNil;
+      i64 vl = 0, vp = 0;
+      u64 vc = 0;
+      if (k < nc) {
+        v = PSLOT(s, np + ntop - 1 - k);  // the chain was recorded bottom-up
+        const NodeRec* r = npeek(v);
+        vl = r->edge_len;
+        vc = r->cmask;
+        vp = r->depth;
+      }
+      wsync();
+      const u32 okc = ballot(k < nc && vp < hS);
+      const int nvc = (okc == kFull) ? kWidth : ffs32(~okc);
+      if (nvc == 0) {
+        fast = false;
+        continue;
+      }
+      const u32 lastc = ballot(k < nvc && vp + vl >= L);
+      const int usedc = lastc ? ffs32(lastc) + 1 : nvc;
+      const i64 mc = min_(vl, L - vp);
+      if (k < usedc) {
+        PSLOT(s, np + k) = v;
+        PM(s, np + k) = (u32)mc;
+        PCM(s, np + k) = vc;
+      }
+      const u32 lc = shfl(v, usedc - 1);
+      const i64 lm = shfl(mc, usedc - 1), lp = shfl(vp, usedc - 1), ll = shfl(vl, usedc - 1);
+      wsync();
+      np += usedc;
       pos = lp + lm;
       cur = lc;
       w.last = lc;
       w.last_m = lm;
-      if (lastm) done = true;  // reached L (or the match ends inside this edge)
+      if (lastc) done = true;
       if (lm < ll) done = true;
-      if (used < 32) fast = false;
       continue;
     }
-#endif
+    // no usable hint: one child-table probe per level
     const i32 t = seq[pos];
-    u32 ch = kNil;
-    const NodeRec* r = nullptr;
-    if (fast && np < nhint) {
-      const u32 c = hint[np];
-      if (c != kNil) {
-        r = nget(c);
-        if (r->parent == cur && r->first_tok == t && r->edge_len > 0) ch = c;
-#if !E2_DEVICE_BUILD
-        else if (r->parent != cur) PHASE_COUNT(6);
-        else PHASE_COUNT(7);
-#endif
-      }
-#if !E2_DEVICE_BUILD
-      else PHASE_COUNT(8);
-#endif
-    }
+    PHASE_COUNT(12);
+    const u32 ch = child_lookup(cur, t);
     if (ch == kNil) {
-      fast = false;
-      PHASE_COUNT(12);
-      ch = child_lookup(cur, t);
-      if (ch == kNil) {
-        w.ok = false;
-        break;
-      }
-      r = nget(ch);
+      w.ok = false;
+      break;
     }
+    const NodeRec* r = nget(ch);
     const i64 len = r->edge_len;
     const i64 m = min_(len, L - pos);
     const u64 cm = r->cmask;
@@ -815,7 +860,7 @@ E2_HD void put_cost(Scr* s, int idx, int g, const CostOut& c) {
 
 // decide (global_scheduler.cpp:76-158).  Warp-wide.  Fills s->c* and
 // s->ratios; w receives the walk for a following commit.
-E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, double now, Walk& w) {
+E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, i64 hS, double now, Walk& w) {
   Dec r;
   r.branch = 1;
   r.gpu = -1;
@@ -847,7 +892,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
   if (lane0()) HOT.stats[kStTreeReads]++;
   wsync();
   PHASE_MARK(1);
-  w = walk_par(seq, L, hint, nhint, s);
+  w = walk_par(seq, L, hint, nhint, s, hS);
   if (!w.ok && s->npath < 0) w = walk_known(seq, L, hint, nhint, s->ext);
   PHASE_MARK(6);
   if (!w.ok) {

@@ -59,6 +59,7 @@ struct SerialArgs {
   const double* arr;
   const i64* outl;
   const i64* L;     // batch-local
+  const i64* S;     // batch-local K1 snapshot match lengths
   const u32* hint;  // batch-local K1 path hints [n][hstride]
   i32 hstride;
   i32 pad2;
@@ -222,7 +223,7 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, int nh, ApiOut* out)
       const bool commit_it = op.kind == OP_SCHEDULE;
       if (commit_it && DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, op.now);
       Walk w;
-      Dec r = decide(s, seq, op.len, op.L, hint, nh, op.now, w);
+      Dec r = decide(s, seq, op.len, op.L, hint, nh, op.L, op.now, w);
       if (!r.ok) return;
       if (commit_it) {
         commit(op.off, op.len, op.L, w, r, op.id, op.arr, op.now, false, s);
@@ -356,7 +357,7 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
   if (DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, now);
   PHASE(0);
   Walk w;
-  Dec dec = decide(s, seq, n, a.L[li], a.hint + li * a.hstride, a.hstride, now, w);
+  Dec dec = decide(s, seq, n, a.L[li], a.hint + li * a.hstride, a.hstride, a.S[li], now, w);
   if (!dec.ok) return;
   PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in

@@ -795,6 +795,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
     g_dev_h = h->d;
     MatchRes m = match_one(d.tok + h->r_off[r], h->r_len[r], h->b_path + w * h->hstride, h->hstride);
     S[w] = m.S;
+    h->b_S[w] = m.S;
     ds[w] = m.div_slot;
     dm[w] = m.div_m;
     h->d_bytes[0] += (unsigned long long)m.bytes;
@@ -1199,10 +1200,10 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     {
       // node cache: as many 4-way sets as fit in ~150 KB of shared memory
       u32 ne = 1;
-#if !defined(E2_NOCACHE)
+#if defined(E2_SMEM_NODECACHE)
       while ((u64)(ne * 2) * (h->d.rs + 12) <= 150u * 1024 && ne * 2 <= 1024) ne *= 2;
 #else
-      ne = kWays;
+      ne = kWays;  // no node cache: the tag arrays stay as a stub
 #endif
       h->nsets = std::max<u32>(ne / kWays, 1);
       const u32 e = h->nsets * kWays;
@@ -1733,6 +1734,7 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     a.arr = d_arr;
     a.outl = d_out;
     a.L = h->b_L;
+    a.S = h->b_S;
     a.hint = h->b_path;
     a.dec = d_dec;
     a.costs = d_cost;
