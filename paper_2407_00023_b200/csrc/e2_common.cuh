@@ -28,6 +28,15 @@
 #define E2_DNI
 #endif
 
+// E2_WARP: the warp-cooperative code paths (32 lanes).  Scalar builds use a
+// width of 1: the host emulation, and the single-thread device engine
+// (E2_SCALAR, e2_serial.cu).
+#if E2_DEVICE_BUILD && !defined(E2_SCALAR)
+#define E2_WARP 1
+#else
+#define E2_WARP 0
+#endif
+
 namespace e2 {
 
 typedef int64_t i64;
@@ -39,7 +48,7 @@ constexpr u32 kNil = 0xffffffffu;
 constexpr u32 kRoot = 0;
 constexpr int kMaxG = 64;
 
-#if E2_DEVICE_BUILD
+#if E2_WARP
 constexpr int kWidth = 32;
 E2_D int lane() { return (int)(threadIdx.x & 31); }
 E2_D void wsync() { __syncwarp(); }
@@ -55,6 +64,26 @@ E2_D int popc64(u64 m) { return __popcll(m); }
 E2_D int ffs64(u64 m) { return __ffsll((long long)m) - 1; }
 // Exact IEEE double ops with explicit rounding so nvcc never contracts a*b+c
 // into an FMA: the reference's bits are computed unfused (SURVEY 7 hard part 4).
+E2_D double dmul(double a, double b) { return __dmul_rn(a, b); }
+E2_D double dadd(double a, double b) { return __dadd_rn(a, b); }
+E2_D double dsub(double a, double b) { return __dsub_rn(a, b); }
+E2_D double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+E2_D double i2d(i64 v) { return __ll2double_rn((long long)v); }
+#elif E2_DEVICE_BUILD
+// single-thread device engine: lane 0 of a width-1 "warp"
+constexpr int kWidth = 1;
+E2_D int lane() { return 0; }
+E2_D void wsync() {}
+E2_D u32 ballot(bool p) { return p ? 1u : 0u; }
+E2_D bool any(bool p) { return p; }
+template <typename T>
+E2_D T shfl(T v, int) { return v; }
+template <typename T>
+E2_D T shfl_up1(T v) { return v; }
+E2_D int ffs32(u32 m) { return __ffs((int)m) - 1; }
+E2_D int popc32(u32 m) { return __popc(m); }
+E2_D int popc64(u64 m) { return __popcll(m); }
+E2_D int ffs64(u64 m) { return __ffsll((long long)m) - 1; }
 E2_D double dmul(double a, double b) { return __dmul_rn(a, b); }
 E2_D double dadd(double a, double b) { return __dadd_rn(a, b); }
 E2_D double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -100,7 +129,7 @@ E2_HD bool lane0() { return lane() == 0; }
 // same 32-wide windows.
 template <typename F>
 E2_D u32 vote(int n, F&& f) {
-#if E2_DEVICE_BUILD
+#if E2_WARP
   const int l = lane();
   return ballot(l < n && f(l));
 #else

@@ -436,7 +436,7 @@ E2_DNI Walk walk_known(const i32* seq, i64 L, const u32* hint, int nhint, i64* e
   return w;
 }
 
-#if E2_DEVICE_BUILD
+#if E2_WARP
 E2_D i64 warp_incl_sum(i64 v) {
   for (int o = 1; o < 32; o <<= 1) {
     const i64 u = (i64)__shfl_up_sync(0xffffffffu, (long long)v, o);
@@ -624,7 +624,7 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
   // extents: a gpu accumulates while every level so far is cached on it;
   // entries exist for the gpus caching the first span
   w.present = np > 0 ? PCM(s, 0) : 0;
-#if E2_DEVICE_BUILD
+#if E2_WARP
   // level-parallel: alive_l = AND of pcm[0..l] (monotone), P_l = matched
   // tokens through level l; gpu g's extent is P at the last level where it
   // is alive, written by the lane of the level where it drops out.
@@ -663,7 +663,7 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
   i64 cl = 0;
   for (int l = lane(); l < np; l += kWidth)
     if (PCM(s, l) != 0) cl += (i64)PM(s, l);
-#if E2_DEVICE_BUILD
+#if E2_WARP
   cl = warp_sum(cl);
 #endif
   w.cached_len = cl;
@@ -710,7 +710,7 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark) {
     PFLAG(s, i) = (newly ? 1u : 0u) | (leaf0 ? 2u : 0u) | (leaf1 ? 4u : 0u) | (fix ? 8u : 0u);
     any |= fix ? 1u : 0u;
   }
-#if E2_DEVICE_BUILD
+#if E2_WARP
   add = warp_sum(add);
   any = ballot(any != 0) ? 1u : 0u;
 #endif
@@ -763,7 +763,7 @@ E2_DNI void update_redirects(Scr* s, double now) {
   }
   // hi / lo: first index of the max / min (strict > / < scans from 0)
   int hi = 0, lo = 0;
-#if E2_DEVICE_BUILD
+#if E2_WARP
   {
     int ih = -1, il = -1;
     double vh = 0, vl = 0;
@@ -804,7 +804,7 @@ E2_DNI void update_redirects(Scr* s, double now) {
 // index with the minimum total among the feasible candidates, else among all.
 // Device: one lane per candidate and a (total, index) warp reduction.
 E2_HD int pick_min(const Scr* s, int n) {
-#if E2_DEVICE_BUILD
+#if E2_WARP
   int bf = -1, ba = -1;  // best feasible / best overall candidate index
   double tf = 0, ta = 0;
   for (int i = lane(); i < n; i += kWidth) {
@@ -911,7 +911,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
     r.branch = 0;
     i64 best = 0;
     u64 cand = 0;
-#if E2_DEVICE_BUILD
+#if E2_WARP
     {
       i64 mine = 0;
       for (int g = lane(); g < G; g += kWidth)

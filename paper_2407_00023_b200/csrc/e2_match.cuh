@@ -22,7 +22,7 @@
 
 namespace e2 {
 
-#if E2_DEVICE_BUILD
+#if E2_WARP
 // Tokens R..R+3 of the 8-token window (x, y): realigns the tree side's
 // 16-byte quads to the prompt's phase (R is the phase difference).
 template <int R>
@@ -94,7 +94,7 @@ E2_D i64 warp_lcp_phase(const int4* A4, const int4* B4, int sb, int dq, i64 lim)
 // realigned to b's phase from the lane's quad and its neighbour's (shfl);
 // the phase difference is warp-uniform, so each phase has its own loop.
 E2_D i64 warp_lcp(const i32* a, const i32* b, i64 lim) {
-#if E2_DEVICE_BUILD
+#if E2_WARP
   if (lim <= 0) return 0;
   const int sb = (int)(((unsigned long long)b >> 2) & 3);
   const int sa = (int)(((unsigned long long)a >> 2) & 3);

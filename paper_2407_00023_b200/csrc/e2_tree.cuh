@@ -58,13 +58,13 @@ E2_HD NodeRec* grec(u32 s) { return (NodeRec*)(DEV.rec + (u64)s * DEV.rs); }
 #if defined(E2_PHASES) && E2_DEVICE_BUILD
 #define PHASE_MARK(i)                                          \
   do {                                                         \
-    __syncwarp();                                              \
+    wsync();                                                   \
     const u64 _pn = clock64();                                 \
     if (lane0()) {                                             \
       HOT.phase_cycles[i] += _pn - HOT.phase_last;             \
       HOT.phase_last = _pn;                                    \
     }                                                          \
-    __syncwarp();                                              \
+    wsync();                                                   \
   } while (0)
 #elif defined(E2_PHASES)
 #include <x86intrin.h>
@@ -120,7 +120,7 @@ E2_D void nflush() {}
 // rec_stride(kMaxG)/8 = 144 words): every load is issued before the first
 // store, so a miss costs one memory latency, not one per 32 words.
 E2_D void rcopy(u64* dst, const u64* src, u32 words) {
-#if E2_DEVICE_BUILD
+#if E2_WARP
   constexpr int kPer = (rec_stride(kMaxG) / 8 + 31) / 32;
   u64 v[kPer];
 #pragma unroll
@@ -244,7 +244,7 @@ E2_DNI Probe ct_probe(u64 key) {
   u64 b = mix64(key) & DEV.ct_mask;
   u64 first_free = ~0ull;
   for (u64 step = 0; step <= DEV.ct_mask; step += 32, b += 32) {
-#if E2_DEVICE_BUILD
+#if E2_WARP
     const CtEntry e = DEV.ct[(b + lane()) & DEV.ct_mask];
     const u32 hit = ballot(e.key == key);
     const u32 emp = ballot(e.key == kEmptyKey);
@@ -254,21 +254,21 @@ E2_DNI Probe ct_probe(u64 key) {
       const int j = ffs32(hit);
       return Probe{(b + (u64)j) & DEV.ct_mask, shfl(e.val, j), true};
     }
+    if (emp) return Probe{first_free, 0, false};
 #else
-    u32 hit = 0, emp = 0, fr = 0;
+    // Scalar: linear probing with early exit.  Same answers as the 32-wide
+    // window: no key ever sits past an empty entry of its probe sequence
+    // (inserts take the first free entry; erases leave tombstones).
     for (int j = 0; j < 32; ++j) {
-      const u64 k = DEV.ct[(b + j) & DEV.ct_mask].key;
-      if (k == key) hit |= 1u << j;
-      if (k == kEmptyKey) emp |= 1u << j;
-      if (k == kEmptyKey || k == kTombKey) fr |= 1u << j;
-    }
-    if (first_free == ~0ull && fr) first_free = (b + (u64)ffs32(fr)) & DEV.ct_mask;
-    if (hit) {
-      const u64 p = (b + (u64)ffs32(hit)) & DEV.ct_mask;
-      return Probe{p, DEV.ct[p].val, true};
+      const u64 p = (b + (u64)j) & DEV.ct_mask;
+      const CtEntry e = DEV.ct[p];
+      if (e.key == key) return Probe{p, e.val, true};
+      if (e.key == kEmptyKey || e.key == kTombKey) {
+        if (first_free == ~0ull) first_free = p;
+        if (e.key == kEmptyKey) return Probe{first_free, 0, false};
+      }
     }
 #endif
-    if (emp) return Probe{first_free, 0, false};
   }
   return Probe{first_free, 0, false};
 }
@@ -339,7 +339,7 @@ E2_HD u64 dring(int g, u32 k) {
 // warp-wide: first directory position whose page max >= key (n if none).
 E2_DNI u32 dir_lower_bound(int g, u64 kla, u64 kid) {
   u32 lo = 0, hi = HOT.dir_n[g];
-#if E2_DEVICE_BUILD
+#if E2_WARP
   while (hi > lo) {
     const u32 step = (hi - lo + 31) / 32;
     const u32 J = (hi - lo + step - 1) / step;
@@ -450,7 +450,7 @@ E2_DNI void dir_remove_at(int g, u32 k) {
 // warp-wide: insert into page p (has room) at directory position k.
 E2_DNI void page_insert(int g, u32 k, u32 p, i32 cnt, u64 kla, u64 kid, u32 slot) {
   const u64 base = (u64)p * kPage;
-#if E2_DEVICE_BUILD
+#if E2_WARP
   const int j = lane();
   const bool valid = j < cnt;
   u64 ela = 0, eid = 0;
@@ -611,7 +611,7 @@ E2_DNI void lru_erase(int g, u64 kla, u64 kid) {
   const u32 p = e.page;
   const i32 cnt = e.cnt;
   const u64 base = (u64)p * kPage;
-#if E2_DEVICE_BUILD
+#if E2_WARP
   const int j = lane();
   const bool valid = j < cnt;
   u64 ela = 0, eid = 0;
