@@ -23,6 +23,7 @@ struct Scr {
   double cL[kMaxG + 1], cM[kMaxG + 1], cP[kMaxG + 1];
   i32 n_costs;
   i32 loads_ok;  // loads[] hold load_ms at this request's `now` (update_redirects ran)
+  i32 spec_bad;  // a speculative decide gave up (see decide)
   i32 npath;  // levels recorded by walk_par (-1: path too deep, sequential fallback)
   // the request's root path, top-down (walk_par / commit)
   u32 pslot[kMaxPath + 1];
@@ -860,7 +861,28 @@ E2_HD void put_cost(Scr* s, int idx, int g, const CostOut& c) {
 
 // decide (global_scheduler.cpp:76-158).  Warp-wide.  Fills s->c* and
 // s->ratios; w receives the walk for a following commit.
-E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, i64 hS, double now, Walk& w) {
+// Warp-wide: does any instance in `set` need the eviction term
+// (missed - free > 0) for this prompt?
+E2_D bool any_need(const Scr* s, u64 set, i64 n) {
+  bool need = false;
+  for (int g = lane(); g < DEV.cfg.G; g += kWidth)
+    if ((set >> g) & 1ull) need |= (n - s->ext[g]) - (DEV.cfg.cap - HOT.cached_tokens[g]) > 0;
+  return any(need);
+}
+
+// decide (global_scheduler.cpp:76-158).  Warp-wide.  Fills s->c* and
+// s->ratios; w receives the walk for a following commit.
+//
+// spec: run concurrently with the eviction warp (two-warp replay).  The
+// decide then changes no shared state and gives up (s->spec_bad) instead of
+// raising an error or evaluating an eviction term (which reads the LRU and
+// hit counters the eviction is changing); the caller validates the result
+// against the nodes the eviction touched and redoes it when needed.  With no
+// eviction term, the cost of instance g depends on the eviction only through
+// need = missed - (cap - cached_tokens[g]) <= 0, which an eviction (cached
+// tokens only decrease) cannot turn positive.
+E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, i64 hS, double now, Walk& w,
+                  bool spec = false) {
   Dec r;
   r.branch = 1;
   r.gpu = -1;
@@ -873,9 +895,20 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
   r.has_ratios = 0;
   r.ok = 1;
   const int G = DEV.cfg.G;
-  if (lane0()) s->n_costs = 0;
+  if (lane0()) {
+    s->n_costs = 0;
+    s->spec_bad = 0;
+  }
   wsync();
+#define SPEC_FAIL()           \
+  do {                        \
+    if (lane0()) s->spec_bad = 1; \
+    wsync();                  \
+    r.ok = 0;                 \
+    return r;                 \
+  } while (0)
   if (n > DEV.cfg.cap) {
+    if (spec) SPEC_FAIL();
     if (lane0()) set_err(kErrNoAdmissible, kWhyPromptTooLong);
     wsync();
     r.ok = 0;
@@ -889,13 +922,17 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
     r.matched = 0;
     return r;
   }
-  if (lane0()) HOT.stats[kStTreeReads]++;
+  if (!spec && lane0()) HOT.stats[kStTreeReads]++;  // a validated speculative decide is counted by the caller
   wsync();
   PHASE_MARK(1);
   w = walk_par(seq, L, hint, nhint, s, hS);
-  if (!w.ok && s->npath < 0) w = walk_known(seq, L, hint, nhint, s->ext);
+  if (!w.ok && s->npath < 0) {
+    if (spec) SPEC_FAIL();
+    w = walk_known(seq, L, hint, nhint, s->ext);
+  }
   PHASE_MARK(6);
   if (!w.ok) {
+    if (spec) SPEC_FAIL();
     if (lane0()) set_err(kErrSim, kWhyWalk);
     wsync();
     r.ok = 0;
@@ -932,6 +969,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
     }
 #endif
     PHASE_MARK(1);
+    if (spec && any_need(s, cand, n)) SPEC_FAIL();
     cost_prepare_set(s, cand, n, now);
     PHASE_MARK(7);
     for (int g = lane(); g < G; g += kWidth) {
@@ -949,6 +987,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
       for (int i = 0; i < nc; ++i)
         if (s->cgpu[i] == t) ti = i;
       if (ti < 0) {
+        if (spec && any_need(s, 1ull << t, n)) SPEC_FAIL();
         cost_prepare(t, n - s->ext[t], now);
         if (lane0()) put_cost(s, nc, t, cost_for(t, n - s->ext[t], now, s));
         wsync();
@@ -985,7 +1024,9 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
       r.gpu = max_g;
     } else {
       r.branch = 1;
-      cost_prepare_set(s, G == 64 ? ~0ull : ((1ull << G) - 1), n, now);
+      const u64 all = G == 64 ? ~0ull : ((1ull << G) - 1);
+      if (spec && any_need(s, all, n)) SPEC_FAIL();
+      cost_prepare_set(s, all, n, now);
       for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(g, n - s->ext[g], now, s));
       wsync();
       if (lane0()) s->n_costs = G;
@@ -993,11 +1034,12 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
       r.gpu = pick_min(s, G);
     }
   }
-  if (HOT.err) {
+  if (!spec && HOT.err) {
     r.ok = 0;
     return r;
   }
   if (r.gpu < 0 || r.gpu >= G) {
+    if (spec) SPEC_FAIL();
     if (lane0()) set_err(kErrSim, kWhyNotContiguous);
     wsync();
     r.ok = 0;
@@ -1005,6 +1047,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
   }
   r.moc = n - s->ext[r.gpu];
   return r;
+#undef SPEC_FAIL
 }
 
 // ---------------------------------------------------------------------------

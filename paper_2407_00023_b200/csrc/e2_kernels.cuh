@@ -341,12 +341,19 @@ E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, int nh, ApiOut* out)
 #define PHASE_T0() PHASE_MARK(15)
 #define PHASE(i) PHASE_MARK(i)
 
-// One request of the generalised criterion-7 loop (e2sched.h, e2_replay).
-E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
+// One request of the generalised criterion-7 loop (e2sched.h, e2_replay),
+// split at the points where the two-warp pipeline hands over:
+//   pre   now + redirect upkeep                  (reads the load windows)
+//   main  decide + commit (+ note_prefill_cached) (the tree, the LRU of g)
+//   post  stats, decision record, note_finished   (windows, inflight map)
+//   evict the driver's eviction notices on g      (LRU of g, cmask, splits)
+// evict(i) commutes with post(i) and pre(i+1): it touches no window or
+// inflight state, so the pipelined replay runs it on a second warp while the
+// first warp continues; main(i+1) waits for it (it reads what evict wrote).
+
+E2_D double replay_pre(Scr* s, const SerialArgs& a, i64 li) {
   const int G = DEV.cfg.G;
   const i64 r = a.base + li;
-  const i64 off = a.off[r], n = a.len[r];
-  const i32* seq = DEV.tok + off;
   PHASE_T0();
   const double now = max_(HOT.drv_now, a.arr[r]);
   if (lane0()) {
@@ -356,29 +363,55 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
   wsync();
   if (DEV.cfg.mode == 0 && DEV.cfg.rebalance && G > 1) update_redirects(s, now);
   PHASE(0);
+  return now;
+}
+
+// spec_w: a speculative decide of this request already validated by the
+// pipeline (its Walk and Scr path are current), or null.
+E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec, const Walk* spec_w = nullptr) {
+  const i64 r = a.base + li;
+  const i64 off = a.off[r], n = a.len[r];
+  const i32* seq = DEV.tok + off;
   Walk w;
-  Dec dec = decide(s, seq, n, a.L[li], a.hint + li * a.hstride, a.hstride, a.S[li], now, w);
-  if (!dec.ok) return;
+  if (spec_w) {
+    w = *spec_w;
+  } else {
+    dec = decide(s, seq, n, a.L[li], a.hint + li * a.hstride, a.hstride, a.S[li], now, w);
+  }
+  if (!dec.ok) return false;
   PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
   const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s);
-  if (HOT.err) return;
+  if (HOT.err) return false;
   PHASE(2);
   if (lane0()) DEV.req_tail[r] = tail;
+  wsync();
+  return true;
+}
+
+E2_D void replay_post(Scr* s, const SerialArgs& a, i64 li, const Dec& dec, double now) {
+  const int G = DEV.cfg.G;
+  const i64 r = a.base + li;
   count_stats(dec);
   write_decision(s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
                  a.ratios ? a.ratios + r * G : nullptr);
   PHASE(3);
-  const int g = dec.gpu;
+  if (li + a.base >= a.lag) {
+    const i64 k = r - a.lag;
+    note_finished(a.ids[k], now, a.outl[k]);
+  }
+  PHASE(5);
+}
 
-  if (HOT.err) return;
+E2_D void replay_evict(const SerialArgs& a, i64 li, int g) {
+  const i64 r = a.base + li;
   if (a.eviction == E2_EVICT_FIFO_TAIL) {
     if (lane0()) {
       u64 t = HOT.fifo_tail[g];
       u64 i = (u64)g * DEV.fcap + (t & (DEV.fcap - 1));
       if (t - HOT.fifo_head[g] >= DEV.fcap) set_err(kErrCapacity, kWhyFifoCap);
       DEV.fifo_req[i] = r;
-      DEV.fifo_tail[i] = n - a.trunk;
+      DEV.fifo_tail[i] = a.len[r] - a.trunk;
       HOT.fifo_tail[g] = t + 1;
     }
     wsync();
@@ -394,30 +427,141 @@ E2_D void replay_step(Scr* s, const SerialArgs& a, i64 li) {
     const i64 cached = HOT.cached_tokens[g];
     if (cached > a.hw && DEV.cfg.mode == 0) evict_lru(g, cached - a.hw);
   }
-  if (HOT.err) return;
   PHASE(4);
-  if (li + a.base >= a.lag) {
-    const i64 k = r - a.lag;
-    note_finished(a.ids[k], now, a.outl[k]);
-  }
-  PHASE(5);
 }
 
-E2_D void serial_body(Scr* s, const SerialArgs& a) {
+// Sequential replay (one warp; the host emulation).
+E2_D void replay_seq(Scr* s, const SerialArgs& a) {
+  i64 i = 0;
+  for (; i < a.n; ++i) {
+    const double now = replay_pre(s, a, i);
+    Dec dec;
+    if (replay_main(s, a, i, now, dec) && !HOT.err) {
+      replay_post(s, a, i, dec, now);
+      if (!HOT.err) replay_evict(a, i, dec.gpu);
+    }
+    if (HOT.err) {
+      if (lane0()) HOT.err_req = a.base + i;
+      wsync();
+      break;
+    }
+  }
+  if (lane0()) HOT.done = i;
+  wsync();
+}
+
+#if E2_WARP
+// Two-warp pipelined replay.  Warp 0 runs pre/main/post; warp 1 runs evict
+// of the previous request meanwhile.  Named barrier 1: warp 1 finished its
+// evict (warp 0 may read the tree/LRU/cmask it wrote); barrier 2: warp 0
+// committed request i and published (i, gpu) — warp 1 may start evict(i).
+struct Pipe {
+  i64 li;
+  i32 g;
+  i32 stop;
+};
+
+E2_D void bar_pair(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+// Warp 0, after barrier 1: did the eviction that ran beside a speculative
+// decide touch any node of the decided path?
+E2_D bool spec_conflict(const Scr* s) {
+  const u32 nt = g_ntouch;
+  if (nt > kTouchCap) return true;
+  const int np = s->npath;
+  if (np < 0) return true;
+  bool hit = false;
+  for (int l = lane(); l < np; l += kWidth) {
+    const u32 v = PSLOT(s, l);
+    for (u32 j = 0; j < nt; ++j) hit |= g_touch[j] == v;
+  }
+  return any(hit);
+}
+
+E2_D void replay_pipe(Scr* s, const SerialArgs& a, Pipe* pp) {
+  if ((threadIdx.x >> 5) == 1) {
+    for (;;) {
+      bar_pair(1);
+      bar_pair(2);
+      if (pp->stop) break;
+      if (lane0()) g_ntouch = 0;
+      wsync();
+      replay_evict(a, pp->li, pp->g);
+    }
+    return;
+  }
+  i64 i = 0, fail = -1;
+  bool past1 = false;  // warp 0 is between barrier 1 and barrier 2
+  for (; i < a.n; ++i) {
+    const double now = replay_pre(s, a, i);
+    // decide speculatively while warp 1 evicts for request i-1
+    Dec dec;
+    Walk w;
+    const bool specd = i > 0;
+    if (specd) {
+      const i64 r = a.base + i;
+      dec = decide(s, DEV.tok + a.off[r], a.len[r], a.L[i], a.hint + i * a.hstride, a.hstride, a.S[i], now, w, true);
+    }
+    PHASE(1);
+    bar_pair(1);
+    past1 = true;
+    PHASE(16);  // waiting for the previous request's eviction
+    if (HOT.err) {  // evict(i-1) failed
+      fail = i - 1;
+      break;
+    }
+    bool ok;
+    if (specd && !s->spec_bad && !spec_conflict(s)) {
+      if (DEV.cfg.mode == 0 && lane0()) HOT.stats[kStTreeReads]++;
+      wsync();
+      ok = replay_main(s, a, i, now, dec, &w);
+    } else {
+      PHASE_COUNT(17);  // speculation redone
+      ok = replay_main(s, a, i, now, dec);
+    }
+    if (!ok || HOT.err) {
+      fail = i;
+      break;
+    }
+    if (lane0()) {
+      pp->li = i;
+      pp->g = dec.gpu;
+      pp->stop = 0;
+    }
+    wsync();
+    bar_pair(2);
+    past1 = false;
+    replay_post(s, a, i, dec, now);
+    if (HOT.err) {
+      fail = i;
+      break;
+    }
+  }
+  if (!past1) bar_pair(1);  // wait for the last evict
+  if (HOT.err && fail < 0) fail = a.n - 1;  // the last evict failed
+  if (lane0()) pp->stop = 1;
+  wsync();
+  bar_pair(2);
+  if (lane0()) {
+    HOT.done = fail < 0 ? a.n : fail;
+    if (fail >= 0) HOT.err_req = a.base + fail;
+  }
+  wsync();
+}
+#endif
+
+E2_D void serial_body(Scr* s, const SerialArgs& a, void* pipe = nullptr) {
   if (lane0()) HOT.done = 0;
   wsync();
   if (a.kind == 0) {
-    i64 i = 0;
-    for (; i < a.n; ++i) {
-      replay_step(s, a, i);
-      if (HOT.err) {
-        if (lane0()) HOT.err_req = a.base + i;
-        wsync();
-        break;
-      }
+#if E2_WARP
+    if (pipe) {
+      replay_pipe(s, a, (Pipe*)pipe);
+      nflush();
+      return;
     }
-    if (lane0()) HOT.done = i;
-    wsync();
+#endif
+    replay_seq(s, a);
   } else {
     api_op(s, a.op, a.hint, a.hstride, a.out);
     if (lane0()) HOT.done = HOT.err ? 0 : 1;

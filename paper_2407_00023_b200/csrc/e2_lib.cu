@@ -125,11 +125,14 @@ constexpr int kMatchWarpsPerBlock = 8;
 constexpr i64 kFirstBatch = 256;  // replay batch-size ramp start
 
 #if E2_DEVICE_BUILD
-__global__ void __launch_bounds__(32, 1) k_serial(SerialArgs a, u32 nsets) {
+// blockDim 32: one warp runs everything; blockDim 64 (replays): the
+// two-warp pipeline of e2_kernels.cuh (warp 1 runs the evictions).
+__global__ void __launch_bounds__(64, 1) k_serial(SerialArgs a, u32 nsets) {
   __shared__ Scr ss;
+  __shared__ Pipe pipe;
   extern __shared__ __align__(16) char dyn[];
   const u32 ne = nsets * kWays;
-  {
+  if (threadIdx.x < 32) {
     const u64* src = (const u64*)g_dev.hot_g;
     u64* dst = (u64*)&g_hot;
     for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
@@ -142,15 +145,15 @@ __global__ void __launch_bounds__(32, 1) k_serial(SerialArgs a, u32 nsets) {
     g_nc.dirty = g_nc.tick + ne;
     g_nc.data = dyn + ((3 * ne * 4 + 15) / 16) * 16;
   }
-  for (u32 i = threadIdx.x; i < ne; i += 32) {
+  for (u32 i = threadIdx.x; i < ne && threadIdx.x < 32; i += 32) {
     ((u32*)dyn)[i] = kNil;
     ((u32*)dyn)[ne + i] = 0;
     ((u32*)dyn)[2 * ne + i] = 0;
   }
-  __syncwarp();
-  serial_body(&ss, a);
-  __syncwarp();
-  {
+  __syncthreads();
+  serial_body(&ss, a, blockDim.x == 64 ? &pipe : nullptr);
+  __syncthreads();
+  if (threadIdx.x < 32) {
     const u64* src = (const u64*)&g_hot;
     u64* dst = (u64*)g_dev.hot_g;
     for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
@@ -321,6 +324,7 @@ struct e2_handle {
   u32* g_tv = nullptr;
   u64 g_mask = 0;
   int n_sm = 148;
+  bool no_pipe = false;  // E2_NO_PIPE=1: single-warp replays (dev comparisons)
   unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions, [2] deepest K1 path beyond the hint stride
   int hstride = kPathHint;             // K1 path hints per request (grown when paths get deeper)
   int want_hstride = kPathHint;
@@ -699,7 +703,14 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
 #if E2_DEVICE_BUILD
     h->acc.launches[a.kind == 0 ? E2_K_COMMIT : E2_K_OTHER]++;
     upload_dev(h);
-    k_serial<<<1, 32, h->serial_smem, h->stream>>>(a, h->nsets);
+    // replays pipeline evictions on a second warp (the shared-memory node
+    // cache variant is single-writer only)
+#if defined(E2_SMEM_NODECACHE)
+    const unsigned threads = 32;
+#else
+    const unsigned threads = (a.kind == 0 && !h->no_pipe) ? 64 : 32;
+#endif
+    k_serial<<<1, threads, h->serial_smem, h->stream>>>(a, h->nsets);
     CK(cudaGetLastError());
 #else
     Scr s;
@@ -1217,6 +1228,8 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
       int dev = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, dev));
+      const char* np = getenv("E2_NO_PIPE");
+      h->no_pipe = np && np[0] == '1';
     }
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream_handle = h->stream;
@@ -1834,7 +1847,7 @@ int e2_profile_reset(e2_handle* h, int32_t enable_timing) {
 extern "C" int e2_debug_phases(e2_handle* h, uint64_t* out) {
   return guard(h, [&] {
     pull_hot(h);
-    for (int i = 0; i < 16; ++i) out[i] = h->hot.phase_cycles[i];
+    for (int i = 0; i < 24; ++i) out[i] = h->hot.phase_cycles[i];
   });
 }
 #endif

@@ -53,6 +53,24 @@ inline NCache g_nc_h;
 
 E2_HD NodeRec* grec(u32 s) { return (NodeRec*)(DEV.rec + (u64)s * DEV.rs); }
 
+// Two-warp pipelined replay (e2_kernels.cuh): the eviction warp (warp 1)
+// records every node whose structure or caching mask it changes, so the
+// decision warp can validate a decide it ran concurrently.
+constexpr u32 kTouchCap = 64;
+#if E2_WARP
+__shared__ u32 g_touch[kTouchCap];
+__shared__ u32 g_ntouch;
+E2_D void touch(u32 v) {
+  if (threadIdx.x >= 32 && lane0()) {
+    const u32 n = g_ntouch;
+    if (n < kTouchCap) g_touch[n] = v;
+    g_ntouch = n + 1;
+  }
+}
+#else
+E2_HD void touch(u32) {}
+#endif
+
 // E2_PHASES (dev-only instrumented builds): cycles since the previous mark
 // are added to phase_cycles[i].  Compiled out of the product.
 #if defined(E2_PHASES) && E2_DEVICE_BUILD
@@ -60,7 +78,7 @@ E2_HD NodeRec* grec(u32 s) { return (NodeRec*)(DEV.rec + (u64)s * DEV.rs); }
   do {                                                         \
     wsync();                                                   \
     const u64 _pn = clock64();                                 \
-    if (lane0()) {                                             \
+    if (lane0() && threadIdx.x < 32) {                         \
       HOT.phase_cycles[i] += _pn - HOT.phase_last;             \
       HOT.phase_last = _pn;                                    \
     }                                                          \
@@ -78,10 +96,17 @@ E2_HD NodeRec* grec(u32 s) { return (NodeRec*)(DEV.rec + (u64)s * DEV.rs); }
 #define PHASE_MARK(i)
 #endif
 #if defined(E2_PHASES)
+#if E2_DEVICE_BUILD
 #define PHASE_COUNT(i)                                         \
   do {                                                         \
-    if (lane0()) HOT.phase_cycles[i] += 1;                     \
+    if (lane0()) atomicAdd((unsigned long long*)&HOT.phase_cycles[i], 1ull); \
   } while (0)
+#else
+#define PHASE_COUNT(i)                                         \
+  do {                                                         \
+    HOT.phase_cycles[i] += 1;                                  \
+  } while (0)
+#endif
 #else
 #define PHASE_COUNT(i)
 #endif
@@ -731,6 +756,8 @@ E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
   }
   const u32 q = node_alloc();
   if (q == kNil) return kNil;
+  touch(s);
+  touch(q);
   const u64 new_id = HOT.next_id;
   const i32 tok_k = DEV.tok[hs.edge_off + k];
   // prefix: copy the whole record (la/hits), then fix header and ccc
@@ -839,6 +866,7 @@ E2_DNI void clear_cached(u32 s, int g) {
   const int G = DEV.cfg.G;
   NodeRec* r = nget(s);
   if (!rcached(r, g)) return;
+  touch(s);
   const u32 p = r->parent;
   const u32 len = r->edge_len;
   if (rleaf(r, s, g, G)) lru_erase(g, dbits(rla(r)[g]), r->id);
