@@ -24,6 +24,7 @@ struct Scr {
   i32 n_costs;
   i32 loads_ok;  // loads[] hold load_ms at this request's `now` (update_redirects ran)
   i32 spec_bad;  // a speculative decide gave up (see decide)
+  i32 fix_D;     // path levels whose LRU fixes path_update_par deferred (0: none)
   i32 npath;  // levels recorded by walk_par (-1: path too deep, sequential fallback)
   // the request's root path, top-down (walk_par / commit)
   u32 pslot[kMaxPath + 1];
@@ -676,7 +677,22 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
 // per node: same final state as the sequential path_update.  Nodes whose
 // LRU membership or key changes are re-indexed afterwards, serially.
 // Warp-wide.
-E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark) {
+// The LRU re-indexing of the path, after path_update_par (deferred variant:
+// run by the eviction warp of the pipelined replay before its eviction).
+E2_DNI void path_lru_fix(const Scr* s, int D, int g) {
+  for (int i = 0; i < D; ++i) {
+    const u32 f = PFLAG(s, i);
+    if (!(f & 8u)) continue;
+    const u32 v = PSLOT(s, i);
+    const NodeRec* r = nget(v);
+    const u64 id = r->id, la1 = dbits(rla(r)[g]);
+    if (f & 2u) lru_erase(g, PLA0(s, i), id);
+    if (f & 4u) lru_insert(g, la1, id, v);
+  }
+}
+
+// defer: leave the LRU re-indexing to path_lru_fix (s->fix_D = D).
+E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark, bool defer = false) {
   const int G = DEV.cfg.G;
   // pass 1: which nodes become cached (a parent's count uses its child's flag)
   for (int i = lane(); i < D; i += kWidth) {
@@ -723,16 +739,11 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark) {
     if (lane0()) rccc(r, G)[g] += 1;
     wsync();
   }
-  if (any) {
-    for (int i = 0; i < D; ++i) {
-      const u32 f = PFLAG(s, i);
-      if (!(f & 8u)) continue;
-      const u32 v = PSLOT(s, i);
-      const NodeRec* r = nget(v);
-      const u64 id = r->id, la1 = dbits(rla(r)[g]);
-      if (f & 2u) lru_erase(g, PLA0(s, i), id);
-      if (f & 4u) lru_insert(g, la1, id, v);
-    }
+  if (defer) {
+    if (lane0()) s->fix_D = any ? D : 0;
+    wsync();
+  } else if (any) {
+    path_lru_fix(s, D, g);
   }
   return D > 0 ? nget(PSLOT(s, 0))->id : 0;
 }
@@ -1144,7 +1155,9 @@ E2_DNI u64 path_update(u32 tail, int g, double now, bool mark) {
 // driver's note_prefill_cached (see path_update).  Warp-wide.  Returns the
 // tail slot.
 E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
-                  double now, bool mark, Scr* s_path) {
+                  double now, bool mark, Scr* s_path, bool defer_lru = false) {
+  if (s_path && lane0()) s_path->fix_D = 0;
+  wsync();
   if (DEV.cfg.mode == 1) {
     if (lane0()) HOT.rr_next++;
     wsync();
@@ -1182,7 +1195,8 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
   }
   u32 plen = kNil;
   if (D >= 0) {
-    root_id = path_update_par(s_path, D, g, now, mark);
+    // levels past kMaxPath live in the single global overflow: not deferrable
+    root_id = path_update_par(s_path, D, g, now, mark, defer_lru && D <= kMaxPath);
     PHASE_MARK(10);
     plen = plog_append(s_path, D, g);
   } else {

@@ -368,7 +368,8 @@ E2_D double replay_pre(Scr* s, const SerialArgs& a, i64 li) {
 
 // spec_w: a speculative decide of this request already validated by the
 // pipeline (its Walk and Scr path are current), or null.
-E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec, const Walk* spec_w = nullptr) {
+E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec, const Walk* spec_w = nullptr,
+                      bool defer_lru = false) {
   const i64 r = a.base + li;
   const i64 off = a.off[r], n = a.len[r];
   const i32* seq = DEV.tok + off;
@@ -381,7 +382,7 @@ E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec,
   if (!dec.ok) return false;
   PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
-  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s);
+  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s, defer_lru);
   if (HOT.err) return false;
   PHASE(2);
   if (lane0()) DEV.req_tail[r] = tail;
@@ -389,13 +390,16 @@ E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec,
   return true;
 }
 
-E2_D void replay_post(Scr* s, const SerialArgs& a, i64 li, const Dec& dec, double now) {
+E2_D void replay_out(const Scr* s, const SerialArgs& a, i64 li, const Dec& dec) {
   const int G = DEV.cfg.G;
   const i64 r = a.base + li;
   count_stats(dec);
   write_decision(s, dec, a.ids[r], a.dec + r, a.costs ? a.costs + r * (G + 1) : nullptr,
                  a.ratios ? a.ratios + r * G : nullptr);
-  PHASE(3);
+}
+
+E2_D void replay_finish(const SerialArgs& a, i64 li, double now) {
+  const i64 r = a.base + li;
   if (li + a.base >= a.lag) {
     const i64 k = r - a.lag;
     note_finished(a.ids[k], now, a.outl[k]);
@@ -437,7 +441,9 @@ E2_D void replay_seq(Scr* s, const SerialArgs& a) {
     const double now = replay_pre(s, a, i);
     Dec dec;
     if (replay_main(s, a, i, now, dec) && !HOT.err) {
-      replay_post(s, a, i, dec, now);
+      replay_out(s, a, i, dec);
+      PHASE(3);
+      replay_finish(a, i, now);
       if (!HOT.err) replay_evict(a, i, dec.gpu);
     }
     if (HOT.err) {
@@ -459,6 +465,8 @@ struct Pipe {
   i64 li;
   i32 g;
   i32 stop;
+  Dec dec;
+  Scr* s;  // the request's scratch (path, costs): double-buffered by warp 0
 };
 
 E2_D void bar_pair(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
@@ -478,7 +486,7 @@ E2_D bool spec_conflict(const Scr* s) {
   return any(hit);
 }
 
-E2_D void replay_pipe(Scr* s, const SerialArgs& a, Pipe* pp) {
+E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
   if ((threadIdx.x >> 5) == 1) {
     for (;;) {
       bar_pair(1);
@@ -486,6 +494,9 @@ E2_D void replay_pipe(Scr* s, const SerialArgs& a, Pipe* pp) {
       if (pp->stop) break;
       if (lane0()) g_ntouch = 0;
       wsync();
+      const Scr* sb = pp->s;
+      if (sb->fix_D > 0) path_lru_fix(sb, sb->fix_D, pp->g);
+      replay_out(sb, a, pp->li, pp->dec);
       replay_evict(a, pp->li, pp->g);
     }
     return;
@@ -493,6 +504,7 @@ E2_D void replay_pipe(Scr* s, const SerialArgs& a, Pipe* pp) {
   i64 i = 0, fail = -1;
   bool past1 = false;  // warp 0 is between barrier 1 and barrier 2
   for (; i < a.n; ++i) {
+    Scr* s = s2 + (i & 1);  // warp 1 reads the other buffer (request i-1) meanwhile
     const double now = replay_pre(s, a, i);
     // decide speculatively while warp 1 evicts for request i-1
     Dec dec;
@@ -514,10 +526,10 @@ E2_D void replay_pipe(Scr* s, const SerialArgs& a, Pipe* pp) {
     if (specd && !s->spec_bad && !spec_conflict(s)) {
       if (DEV.cfg.mode == 0 && lane0()) HOT.stats[kStTreeReads]++;
       wsync();
-      ok = replay_main(s, a, i, now, dec, &w);
+      ok = replay_main(s, a, i, now, dec, &w, true);
     } else {
       PHASE_COUNT(17);  // speculation redone
-      ok = replay_main(s, a, i, now, dec);
+      ok = replay_main(s, a, i, now, dec, nullptr, true);
     }
     if (!ok || HOT.err) {
       fail = i;
@@ -527,11 +539,13 @@ E2_D void replay_pipe(Scr* s, const SerialArgs& a, Pipe* pp) {
       pp->li = i;
       pp->g = dec.gpu;
       pp->stop = 0;
+      pp->dec = dec;
+      pp->s = s;
     }
     wsync();
     bar_pair(2);
     past1 = false;
-    replay_post(s, a, i, dec, now);
+    replay_finish(a, i, now);
     if (HOT.err) {
       fail = i;
       break;

@@ -122,15 +122,19 @@ void grow(T*& p, size_t keep, size_t n, Stream s) {
 namespace {
 
 constexpr int kMatchWarpsPerBlock = 8;
-constexpr i64 kFirstBatch = 256;  // replay batch-size ramp start
+constexpr i64 kFirstBatch = 2048;  // replay batch-size ramp start
+constexpr size_t kScrBytes = (2 * sizeof(Scr) + 127) / 128 * 128;
 
 #if E2_DEVICE_BUILD
 // blockDim 32: one warp runs everything; blockDim 64 (replays): the
 // two-warp pipeline of e2_kernels.cuh (warp 1 runs the evictions).
+// Dynamic shared memory: two Scr buffers (the pipeline alternates them per
+// request), then the node-cache arrays (a stub unless E2_SMEM_NODECACHE).
 __global__ void __launch_bounds__(64, 1) k_serial(SerialArgs a, u32 nsets) {
-  __shared__ Scr ss;
   __shared__ Pipe pipe;
-  extern __shared__ __align__(16) char dyn[];
+  extern __shared__ __align__(16) char dyn0[];
+  Scr* ss = (Scr*)dyn0;
+  char* dyn = dyn0 + kScrBytes;
   const u32 ne = nsets * kWays;
   if (threadIdx.x < 32) {
     const u64* src = (const u64*)g_dev.hot_g;
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(64, 1) k_serial(SerialArgs a, u32 nsets) {
     ((u32*)dyn)[2 * ne + i] = 0;
   }
   __syncthreads();
-  serial_body(&ss, a, blockDim.x == 64 ? &pipe : nullptr);
+  serial_body(ss, a, blockDim.x == 64 ? &pipe : nullptr);
   __syncthreads();
   if (threadIdx.x < 32) {
     const u64* src = (const u64*)&g_hot;
@@ -1218,7 +1222,7 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
 #endif
       h->nsets = std::max<u32>(ne / kWays, 1);
       const u32 e = h->nsets * kWays;
-      h->serial_smem = ((3 * e * 4 + 15) / 16) * 16 + (size_t)e * h->d.rs;
+      h->serial_smem = kScrBytes + ((3 * e * 4 + 15) / 16) * 16 + (size_t)e * h->d.rs;
     }
 #if E2_DEVICE_BUILD
     CK(cudaFuncSetAttribute(k_serial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->serial_smem));
