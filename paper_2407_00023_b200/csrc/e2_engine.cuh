@@ -627,6 +627,23 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
   // entries exist for the gpus caching the first span
   w.present = np > 0 ? PCM(s, 0) : 0;
 #if E2_WARP
+  if (np <= 8 && G <= 32) {
+    // shallow path: lane g walks the levels itself (no scans); every lane
+    // also sums cached_len redundantly, so no reduction is needed
+    i64 e = 0, cl = 0;
+    bool alive = lane() < G && ((w.present >> lane()) & 1ull);
+    for (int l = 0; l < np; ++l) {
+      const u64 cm = s->pcm[l];
+      const i64 m = (i64)s->pm[l];
+      alive = alive && ((cm >> lane()) & 1ull);
+      if (alive) e += m;
+      if (cm != 0) cl += m;
+    }
+    if (lane() < G) s->ext[lane()] = e;
+    w.cached_len = cl;
+    wsync();
+    return w;
+  }
   // level-parallel: alive_l = AND of pcm[0..l] (monotone), P_l = matched
   // tokens through level l; gpu g's extent is P at the last level where it
   // is alive, written by the lane of the level where it drops out.
@@ -784,14 +801,16 @@ E2_DNI void update_redirects(Scr* s, double now) {
       if (ih < 0 || v > vh) { vh = v; ih = g; }
       if (il < 0 || v < vl) { vl = v; il = g; }
     }
-    for (int o = 16; o; o >>= 1) {
+    // lanes [0, gtop) hold every instance (g and g+32 share a lane): an
+    // xor butterfly over gtop lanes, then lane 0's answer to all
+    for (int o = DEV.cfg.gtop >> 1; o; o >>= 1) {
       const double wh = __shfl_xor_sync(0xffffffffu, vh, o), wl = __shfl_xor_sync(0xffffffffu, vl, o);
       const int jh = __shfl_xor_sync(0xffffffffu, ih, o), jl = __shfl_xor_sync(0xffffffffu, il, o);
       if (jh >= 0 && (ih < 0 || wh > vh || (wh == vh && jh < ih))) { vh = wh; ih = jh; }
       if (jl >= 0 && (il < 0 || wl < vl || (wl == vl && jl < il))) { vl = wl; il = jl; }
     }
-    hi = ih;
-    lo = il;
+    hi = shfl(ih, 0);
+    lo = shfl(il, 0);
   }
 #else
   for (int g = 1; g < G; ++g) {
@@ -824,13 +843,22 @@ E2_HD int pick_min(const Scr* s, int n) {
     if (!s->cinf[i] && (bf < 0 || t < tf)) { tf = t; bf = i; }
     if (ba < 0 || t < ta) { ta = t; ba = i; }
   }
-  for (int o = 16; o; o >>= 1) {
-    const double uf = __shfl_xor_sync(0xffffffffu, tf, o), ua = __shfl_xor_sync(0xffffffffu, ta, o);
-    const int jf = __shfl_xor_sync(0xffffffffu, bf, o), ja = __shfl_xor_sync(0xffffffffu, ba, o);
-    if (jf >= 0 && (bf < 0 || uf < tf || (uf == tf && jf < bf))) { tf = uf; bf = jf; }
-    if (ja >= 0 && (ba < 0 || ua < ta || (ua == ta && ja < ba))) { ta = ua; ba = ja; }
+  // candidates sit in lanes [0, top), top = pow2 >= min(n, 32)
+  int top = 1;
+  while (top < n && top < 32) top <<= 1;
+  const bool anyf = any(bf >= 0);
+  for (int o = top >> 1; o; o >>= 1) {
+    if (anyf) {
+      const double uf = __shfl_xor_sync(0xffffffffu, tf, o);
+      const int jf = __shfl_xor_sync(0xffffffffu, bf, o);
+      if (jf >= 0 && (bf < 0 || uf < tf || (uf == tf && jf < bf))) { tf = uf; bf = jf; }
+    } else {
+      const double ua = __shfl_xor_sync(0xffffffffu, ta, o);
+      const int ja = __shfl_xor_sync(0xffffffffu, ba, o);
+      if (ja >= 0 && (ba < 0 || ua < ta || (ua == ta && ja < ba))) { ta = ua; ba = ja; }
+    }
   }
-  const int b = bf >= 0 ? bf : ba;
+  const int b = shfl(anyf ? bf : ba, 0);
   return b >= 0 ? s->cgpu[b] : -1;
 #else
   int best = -1;
@@ -964,8 +992,8 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
       i64 mine = 0;
       for (int g = lane(); g < G; g += kWidth)
         if ((w.present >> g) & 1ull) mine = max_(mine, s->ext[g]);
-      for (int o = 16; o; o >>= 1) mine = max_(mine, (i64)__shfl_xor_sync(0xffffffffu, (long long)mine, o));
-      best = mine;
+      for (int o = DEV.cfg.gtop >> 1; o; o >>= 1) mine = max_(mine, (i64)__shfl_xor_sync(0xffffffffu, (long long)mine, o));
+      best = shfl(mine, 0);
       for (int b = 0; b < G; b += 32) {
         const int g = b + lane();
         const bool c = g < G && ((w.present >> g) & 1ull) && s->ext[g] == best;

@@ -1195,6 +1195,8 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     Cfg c;
     memset(&c, 0, sizeof(c));
     c.G = n_gpus;
+    c.gtop = 1;
+    while (c.gtop < std::min(n_gpus, 32)) c.gtop *= 2;
     c.mode = policy->mode == E2_MODE_ROUND_ROBIN ? 1 : 0;
     c.rebalance = policy->rebalance;
     c.autoscale = policy->autoscale;

@@ -138,7 +138,7 @@ struct Cfg {
   i32 G;
   i32 mode;  // 0 prefix-aware, 1 round robin
   i32 rebalance, autoscale, pd_balance;
-  i32 pad;
+  i32 gtop;  // power of two >= min(G, 32): xor-reduction span over per-instance lanes
   double H, th_bal, imbal;
   i64 cap, default_out;
   double c0, c1, c2, c3;
