@@ -25,6 +25,7 @@ struct Scr {
   i32 loads_ok;  // loads[] hold load_ms at this request's `now` (update_redirects ran)
   i32 spec_bad;  // a speculative decide gave up (see decide)
   i32 fix_D;     // path levels whose LRU fixes path_update_par deferred (0: none)
+  i32 cpath;     // levels of the committed path in pslot (-1: not recorded)
   i32 npath;  // levels recorded by walk_par (-1: path too deep, sequential fallback)
   // the request's root path, top-down (walk_par / commit)
   u32 pslot[kMaxPath + 1];
@@ -462,7 +463,13 @@ E2_D i64 warp_sum(i64 v) {
 // hS: K1's snapshot match length.  A hinted slot is on this prompt's path
 // only while its (current) start lies below hS: the last hint may be a node
 // K1 matched only partially, whose slot now holds the part past hS.
-E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, i64 hS) {
+// Leader hints: the committed path of the request's in-batch leader (LCP =
+// L), used past the point where its own K1 hints end (bound L instead of
+// hS).  lead points at the request's leader index (-1: none); the leader's
+// row is hint_rows + leader * nhint.  Read only when needed.
+E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, i64 hS,
+                     const i64* lead = nullptr, const u32* hint_rows = nullptr) {
+  const u32* hint2 = nullptr;
   Walk w;
   w.last = kRoot;
   w.last_m = 0;
@@ -539,60 +546,95 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
       const u32 p0 = shfl(par, 0);
       const i64 l0 = shfl(len, 0);
       if (!in0 || l0 == 0 || p0 == cur || p0 == kNil) {
+        if (lead && !hint2) {
+          const i64 ld = *lead;
+          hint2 = ld >= 0 ? hint_rows + ld * (i64)nhint : hint;
+        }
+        if (hint2 && hint != hint2) {
+          // switch to the leader's committed path: its entries starting at or
+          // after `pos` continue this prompt's path (both share [0, L))
+          hint = hint2;
+          hS = L;
+          int idx = min_(np, nhint - 1);
+          while (idx > 0) {
+            const u32 c2 = hint[idx - 1];
+            if (c2 == kNil || npeek(c2)->depth >= pos) --idx;
+            else break;
+          }
+          while (idx < nhint - 1) {
+            const u32 c2 = hint[idx];
+            if (c2 != kNil && npeek(c2)->depth < pos) ++idx;
+            else break;
+          }
+          hi = idx;
+          PHASE_COUNT(18);
+          continue;
+        }
+        if (hint == hint2) PHASE_COUNT(19);
         fast = false;
         continue;
       }
       int nc = 0;
       u32 x = p0;
-      while (x != cur && x != kRoot && x != kNil && nc < 32 && np + nc < kPathLevels) {
+      while (x != cur && x != kRoot && x != kNil && np + nc < kPathLevels) {
         if (lane0()) PSLOT(s, np + nc) = x;
         nc++;
         x = npeek(x)->parent;
       }
       wsync();
       if (x != cur || nc == 0) {
+        PHASE_COUNT(20);
         fast = false;
         continue;
       }
-      // take up to kWidth levels from the top of the chain (the rest, if
-      // any, is climbed again on the next pass)
-      const int ntop = nc;
-      nc = min_(nc, kWidth);
-      u32 v = kNil;
-      i64 vl = 0, vp = 0;
-      u64 vc = 0;
-      if (k < nc) {
-        v = PSLOT(s, np + ntop - 1 - k);  // the chain was recorded bottom-up
-        const NodeRec* r = npeek(v);
-        vl = r->edge_len;
-        vc = r->cmask;
-        vp = r->depth;
+      // the chain was recorded bottom-up: reverse it in place, then take its
+      // levels top-down, kWidth per step, while they start below hS
+      for (int j = lane(); j < nc / 2; j += kWidth) {
+        const u32 t0 = PSLOT(s, np + j), t1 = PSLOT(s, np + nc - 1 - j);
+        PSLOT(s, np + j) = t1;
+        PSLOT(s, np + nc - 1 - j) = t0;
       }
       wsync();
-      const u32 okc = ballot(k < nc && vp < hS);
-      const int nvc = (okc == kFull) ? kWidth : ffs32(~okc);
-      if (nvc == 0) {
-        fast = false;
-        continue;
+      for (int c0 = 0; c0 < nc && !done;) {
+        const int j = c0 + k, chunk = min_(nc - c0, kWidth);
+        u32 v = kNil;
+        i64 vl = 0, vp = 0;
+        u64 vc = 0;
+        if (k < chunk) {
+          v = PSLOT(s, np + k);
+          const NodeRec* r = npeek(v);
+          vl = r->edge_len;
+          vc = r->cmask;
+          vp = r->depth;
+        }
+        (void)j;
+        const u32 okc = ballot(k < chunk && vp < hS);
+        const int nvc = (okc == kFull) ? kWidth : ffs32(~okc);
+        if (nvc == 0) {
+          PHASE_COUNT(21);
+          fast = false;
+          break;
+        }
+        const u32 lastc = ballot(k < nvc && vp + vl >= L);
+        const int usedc = lastc ? ffs32(lastc) + 1 : nvc;
+        const i64 mc = min_(vl, L - vp);
+        if (k < usedc) {
+          PM(s, np + k) = (u32)mc;
+          PCM(s, np + k) = vc;
+        }
+        const u32 lc = shfl(v, usedc - 1);
+        const i64 lm = shfl(mc, usedc - 1), lp = shfl(vp, usedc - 1), ll = shfl(vl, usedc - 1);
+        wsync();
+        np += usedc;
+        c0 += usedc;
+        pos = lp + lm;
+        cur = lc;
+        w.last = lc;
+        w.last_m = lm;
+        if (lastc) done = true;
+        if (lm < ll) done = true;
+        if (usedc < chunk) break;  // a chain node starts past hS: re-evaluated next pass
       }
-      const u32 lastc = ballot(k < nvc && vp + vl >= L);
-      const int usedc = lastc ? ffs32(lastc) + 1 : nvc;
-      const i64 mc = min_(vl, L - vp);
-      if (k < usedc) {
-        PSLOT(s, np + k) = v;
-        PM(s, np + k) = (u32)mc;
-        PCM(s, np + k) = vc;
-      }
-      const u32 lc = shfl(v, usedc - 1);
-      const i64 lm = shfl(mc, usedc - 1), lp = shfl(vp, usedc - 1), ll = shfl(vl, usedc - 1);
-      wsync();
-      np += usedc;
-      pos = lp + lm;
-      cur = lc;
-      w.last = lc;
-      w.last_m = lm;
-      if (lastc) done = true;
-      if (lm < ll) done = true;
       continue;
     }
     // no usable hint: one child-table probe per level
@@ -921,7 +963,7 @@ E2_D bool any_need(const Scr* s, u64 set, i64 n) {
 // need = missed - (cap - cached_tokens[g]) <= 0, which an eviction (cached
 // tokens only decrease) cannot turn positive.
 E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, i64 hS, double now, Walk& w,
-                  bool spec = false) {
+                  bool spec = false, const i64* lead = nullptr, const u32* hint_rows = nullptr) {
   Dec r;
   r.branch = 1;
   r.gpu = -1;
@@ -964,7 +1006,7 @@ E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhi
   if (!spec && lane0()) HOT.stats[kStTreeReads]++;  // a validated speculative decide is counted by the caller
   wsync();
   PHASE_MARK(1);
-  w = walk_par(seq, L, hint, nhint, s, hS);
+  w = walk_par(seq, L, hint, nhint, s, hS, lead, hint_rows);
   if (!w.ok && s->npath < 0) {
     if (spec) SPEC_FAIL();
     w = walk_known(seq, L, hint, nhint, s->ext);
@@ -1184,7 +1226,10 @@ E2_DNI u64 path_update(u32 tail, int g, double now, bool mark) {
 // tail slot.
 E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
                   double now, bool mark, Scr* s_path, bool defer_lru = false) {
-  if (s_path && lane0()) s_path->fix_D = 0;
+  if (s_path && lane0()) {
+    s_path->fix_D = 0;
+    s_path->cpath = -1;
+  }
   wsync();
   if (DEV.cfg.mode == 1) {
     if (lane0()) HOT.rr_next++;
@@ -1223,6 +1268,7 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
   }
   u32 plen = kNil;
   if (D >= 0) {
+    if (lane0()) s_path->cpath = D;
     // levels past kMaxPath live in the single global overflow: not deferrable
     root_id = path_update_par(s_path, D, g, now, mark, defer_lru && D <= kMaxPath);
     PHASE_MARK(10);

@@ -60,7 +60,9 @@ struct SerialArgs {
   const i64* outl;
   const i64* L;     // batch-local
   const i64* S;     // batch-local K1 snapshot match lengths
-  const u32* hint;  // batch-local K1 path hints [n][hstride]
+  const i64* lead;  // batch-local in-batch leader (LCP = L) or -1
+  u32* hint;        // batch-local K1 path hints [n][hstride]; a committed request's row is
+                    // rewritten with its committed path (the hints of its in-batch followers)
   i32 hstride;
   i32 pad2;
   e2_decision* dec;
@@ -377,7 +379,8 @@ E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec,
   if (spec_w) {
     w = *spec_w;
   } else {
-    dec = decide(s, seq, n, a.L[li], a.hint + li * a.hstride, a.hstride, a.S[li], now, w);
+    dec = decide(s, seq, n, a.L[li], a.hint + li * a.hstride, a.hstride, a.S[li], now, w, false,
+                 a.lead ? a.lead + li : nullptr, a.hint);
   }
   if (!dec.ok) return false;
   PHASE(1);
@@ -386,6 +389,14 @@ E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec,
   if (HOT.err) return false;
   PHASE(2);
   if (lane0()) DEV.req_tail[r] = tail;
+  // this request's hint row now holds its committed path: the hints of the
+  // later requests of the batch that extend it (leader rounds)
+  const int D = s->cpath;
+  if (D >= 0) {
+    u32* row = a.hint + li * a.hstride;
+    const int nw = min_(D, a.hstride - 1);
+    for (int l = lane(); l <= nw; l += kWidth) row[l] = l < nw ? PSLOT(s, l) : kNil;
+  }
   wsync();
   return true;
 }
@@ -512,7 +523,8 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     const bool specd = i > 0;
     if (specd) {
       const i64 r = a.base + i;
-      dec = decide(s, DEV.tok + a.off[r], a.len[r], a.L[i], a.hint + i * a.hstride, a.hstride, a.S[i], now, w, true);
+      dec = decide(s, DEV.tok + a.off[r], a.len[r], a.L[i], a.hint + i * a.hstride, a.hstride, a.S[i], now, w, true,
+                   a.lead ? a.lead + i : nullptr, a.hint);
     }
     PHASE(1);
     bar_pair(1);

@@ -221,11 +221,12 @@ __device__ __forceinline__ u32 gtab_find(const u64* tk, const u32* tv, u64 mask,
 
 __global__ void k_group_init(i64 n, i64 base, const i64* off, const i64* len, const i64* S, const u32* dslot,
                              const u32* dm, i32* state, u64* A, u64* B, i64* cand, i64* L, u64* tk, u32* tv,
-                             u64 mask) {
+                             u64 mask, i64* leader) {
   i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const i64 r = base + i;
   const i64 s = S[i];
+  leader[i] = -1;  // the final leader (LCP = L) of a request extended by the rounds
   if (s >= len[r]) {
     state[i] = 0;
     L[i] = s;
@@ -769,6 +770,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   if (n == 1) {
     // single sequence: no intra-batch dependency
     d2d(h->b_L, h->b_S, 8, h->stream);
+    dset(h->b_leader, 0xff, 8, h->stream);  // -1: no in-batch leader
     return;
   }
   Timed t(h, E2_K_GROUP);
@@ -778,7 +780,8 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   dset(h->g_tv, 0xff, tsz * 4, h->stream);
   h->acc.launches[E2_K_GROUP]++;
   k_group_init<<<tg, 256, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot, h->b_dm, h->b_state,
-                                          h->b_A, h->b_B, h->b_cand, h->b_L, h->g_tk, h->g_tv, h->g_mask);
+                                          h->b_A, h->b_B, h->b_cand, h->b_L, h->g_tk, h->g_tv, h->g_mask,
+                                          h->b_leader);
   CK(cudaGetLastError());
   for (int round = 0;; ++round) {
     dset(h->d_cnt, 0, 8, h->stream);
@@ -820,7 +823,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
   // leader rounds with std::map grouping (same recursion as the device)
   std::vector<i32> st(n);
   std::vector<u64> A(n), B(n);
-  std::vector<i64> cand(n), leader(n), o(n);
+  std::vector<i64> cand(n), leader(n, -1), o(n);
   i64* L = h->b_L;
   for (i64 i = 0; i < n; ++i) {
     const i64 r = base + i;
@@ -867,6 +870,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
       }
     }
   }
+  for (i64 i = 0; i < n; ++i) h->b_leader[i] = leader[i];
 #endif
 }
 
@@ -1754,6 +1758,7 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     a.outl = d_out;
     a.L = h->b_L;
     a.S = h->b_S;
+    a.lead = h->b_leader;
     a.hint = h->b_path;
     a.dec = d_dec;
     a.costs = d_cost;

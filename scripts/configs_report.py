@@ -37,12 +37,22 @@ def main(names):
         cpu = time.perf_counter() - t0
         bb = type(b)(b.decisions[:trr.n], b.costs[:trr.n], None, min(b.n_done, trr.n))
         d = diff_decisions(a, bb)
+        # the product on exactly the reference's prefix (same work on both sides)
+        same = None
+        if trr.n < tr.n:
+            prod.e2_reset(s._h)
+            prod.e2_profile_reset(s._h, 1)
+            s.replay(trr, cfg.driver)
+            p2 = abi.ProfileC()
+            prod.e2_profile_get(s._h, ctypes.byref(p2))
+            same = trr.n / (sum(p2.ms) / 1000)
         print(json.dumps({
             "config": cfg.name, "requests": tr.n, "instances": cfg.n_gpus,
             "b200_decisions_per_s_kernel": tr.n / (kms / 1000), "b200_decisions_per_s_wall": tr.n / wall,
             "kernel_ms": {k: prof.ms[i] for i, k in enumerate(["match", "group", "serial", "other"])},
             "match_gbps": (prof.match_bytes / 1e9) / (prof.ms[0] / 1e3) if prof.ms[0] else None,
             "reference_requests": trr.n, "reference_decisions_per_s": trr.n / cpu,
+            "b200_decisions_per_s_on_reference_prefix": same if same is not None else tr.n / (kms / 1000),
             "bit_exact_on_reference_prefix": d is None, "first_mismatch": d,
             "nodes": s.node_count(),
         }), flush=True)
