@@ -76,6 +76,8 @@ struct InfRec {
   u64 pad2;
 };
 
+static_assert(sizeof(InfRec) % 8 == 0, "inflight records are copied as 8-byte words");
+
 struct WinEnt {
   double t;
   i64 missed;
