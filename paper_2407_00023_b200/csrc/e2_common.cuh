@@ -123,6 +123,11 @@ inline double i2d(i64 v) { return (double)v; }
 #endif
 
 E2_HD bool lane0() { return lane() == 0; }
+#if E2_DEVICE_BUILD
+E2_D bool thread0() { return threadIdx.x == 0; }  // lane 0 of warp 0
+#else
+inline bool thread0() { return true; }
+#endif
 
 // Warp vote over positions [0, n) (n <= 32): bit j = f(j).  On the device
 // lane j evaluates f(j); the host emulation loops, so both builds probe the

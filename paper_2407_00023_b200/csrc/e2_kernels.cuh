@@ -497,7 +497,88 @@ E2_D bool spec_conflict(const Scr* s) {
   return any(hit);
 }
 
+// Warp 2 (optional): an L1 prefetcher running one request ahead of warp 0.
+// It only issues prefetches for addresses the next request will probably
+// touch — its hint-path records, the prompt token at L and the child-table
+// window of the leaf it will insert, the inflight slots of its insert and of
+// the note_finished of its step, each instance's window head and LRU head
+// victim — so a race with the writers can only cost a useless prefetch.
+__shared__ volatile long long g_pf_cur;
+__shared__ volatile int g_pf_stop;
+
+E2_D void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+E2_D void prefetch_request(const SerialArgs& a, i64 j) {
+  const int G = DEV.cfg.G;
+  const i64 r = a.base + j;
+  const i64 off = a.off[r], n = a.len[r], L = a.L[j];
+  const u32* row = a.hint + j * a.hstride;
+  const u32 c = row[lane()];
+  const u32 nilm = ballot(c == kNil);
+  const int nh = nilm ? ffs32(nilm) : 32;
+  if (lane() < nh && c < DEV.node_cap) {
+    const char* rec = (const char*)grec(c);
+    pf(rec);
+    if (DEV.rs > 128) pf(rec + 128);
+  }
+  const u32 last = nh > 0 ? shfl(c, nh - 1) : kRoot;
+  if (L < n) {
+    const i32 t = DEV.tok[off + L];
+    const u64 b = mix64(ckey(last, t)) & DEV.ct_mask;
+    if (lane() < 4) pf(&DEV.ct[(b + 8 * lane()) & DEV.ct_mask]);
+  }
+  if (lane() == 4) {
+    const u64 h = mix64((u64)a.ids[r]) & DEV.inf_mask;
+    pf(&DEV.inf[h]);
+    pf(&DEV.inf[(h + 2) & DEV.inf_mask]);
+  }
+  if (lane() == 5 && j + a.base >= a.lag) {
+    const u64 h = mix64((u64)a.ids[r - a.lag]) & DEV.inf_mask;
+    pf(&DEV.inf[h]);
+    pf(&DEV.inf[(h + 2) & DEV.inf_mask]);
+  }
+  for (int g = lane(); g < G; g += kWidth) {
+    pf(&DEV.win[wslot(g, HOT.ws_head[g])]);
+    if (HOT.dir_n[g] > 0) {
+      const DirEntry e = DEV.dir[dring(g, 0)];
+      if (e.page < DEV.page_cap) {
+        const u64 pi = (u64)e.page * kPage;
+        pf(&DEV.pg_la[pi]);
+        pf(&DEV.pg_id[pi]);
+        const u32 v = DEV.pg_slot[pi];
+        if (v < DEV.node_cap) {
+          const char* rec = (const char*)grec(v);
+          pf(rec);
+          pf(rec + 128);
+          const NodeRec* rv = (const NodeRec*)rec;
+          const u32 p = rv->parent;
+          if (p < DEV.node_cap) pf(grec(p));
+        }
+      }
+      pf(&DEV.dir[dring(g, HOT.dir_n[g] - 1)]);
+    }
+  }
+}
+
+E2_D void prefetch_loop(const SerialArgs& a) {
+  i64 done = -1;
+  while (!g_pf_stop) {
+    const i64 cur = g_pf_cur;
+    const i64 want = min_<i64>(cur + 1, a.n - 1);
+    if (done >= want) {
+      __nanosleep(256);
+      continue;
+    }
+    done = max_<i64>(done + 1, cur + 1);
+    prefetch_request(a, done);
+  }
+}
+
 E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
+  if ((threadIdx.x >> 5) == 2) {
+    prefetch_loop(a);
+    return;
+  }
   if ((threadIdx.x >> 5) == 1) {
     for (;;) {
       bar_pair(1);
@@ -516,6 +597,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
   bool past1 = false;  // warp 0 is between barrier 1 and barrier 2
   for (; i < a.n; ++i) {
     Scr* s = s2 + (i & 1);  // warp 1 reads the other buffer (request i-1) meanwhile
+    if (lane0()) g_pf_cur = i;
     const double now = replay_pre(s, a, i);
     // decide speculatively while warp 1 evicts for request i-1
     Dec dec;
@@ -565,7 +647,10 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
   }
   if (!past1) bar_pair(1);  // wait for the last evict
   if (HOT.err && fail < 0) fail = a.n - 1;  // the last evict failed
-  if (lane0()) pp->stop = 1;
+  if (lane0()) {
+    pp->stop = 1;
+    g_pf_stop = 1;
+  }
   wsync();
   bar_pair(2);
   if (lane0()) {
@@ -577,7 +662,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
 #endif
 
 E2_D void serial_body(Scr* s, const SerialArgs& a, void* pipe = nullptr) {
-  if (lane0()) HOT.done = 0;
+  if (thread0()) HOT.done = 0;
   wsync();
   if (a.kind == 0) {
 #if E2_WARP

@@ -130,7 +130,7 @@ constexpr size_t kScrBytes = (2 * sizeof(Scr) + 127) / 128 * 128;
 // two-warp pipeline of e2_kernels.cuh (warp 1 runs the evictions).
 // Dynamic shared memory: two Scr buffers (the pipeline alternates them per
 // request), then the node-cache arrays (a stub unless E2_SMEM_NODECACHE).
-__global__ void __launch_bounds__(64, 1) k_serial(SerialArgs a, u32 nsets) {
+__global__ void __launch_bounds__(96, 1) k_serial(SerialArgs a, u32 nsets) {
   __shared__ Pipe pipe;
   extern __shared__ __align__(16) char dyn0[];
   Scr* ss = (Scr*)dyn0;
@@ -154,8 +154,12 @@ __global__ void __launch_bounds__(64, 1) k_serial(SerialArgs a, u32 nsets) {
     ((u32*)dyn)[ne + i] = 0;
     ((u32*)dyn)[2 * ne + i] = 0;
   }
+  if (threadIdx.x == 0) {
+    g_pf_cur = -1;
+    g_pf_stop = 0;
+  }
   __syncthreads();
-  serial_body(ss, a, blockDim.x == 64 ? &pipe : nullptr);
+  serial_body(ss, a, blockDim.x >= 64 ? &pipe : nullptr);
   __syncthreads();
   if (threadIdx.x < 32) {
     const u64* src = (const u64*)&g_hot;
@@ -329,7 +333,8 @@ struct e2_handle {
   u32* g_tv = nullptr;
   u64 g_mask = 0;
   int n_sm = 148;
-  bool no_pipe = false;  // E2_NO_PIPE=1: single-warp replays (dev comparisons)
+  bool no_pipe = false;      // E2_NO_PIPE=1: single-warp replays (dev comparisons)
+  bool no_prefetch = false;  // E2_NO_PREFETCH=1: no prefetch warp (dev comparisons)
   unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions, [2] deepest K1 path beyond the hint stride
   int hstride = kPathHint;             // K1 path hints per request (grown when paths get deeper)
   int want_hstride = kPathHint;
@@ -713,7 +718,7 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
 #if defined(E2_SMEM_NODECACHE)
     const unsigned threads = 32;
 #else
-    const unsigned threads = (a.kind == 0 && !h->no_pipe) ? 64 : 32;
+    const unsigned threads = (a.kind == 0 && !h->no_pipe) ? (h->no_prefetch ? 64 : 96) : 32;
 #endif
     k_serial<<<1, threads, h->serial_smem, h->stream>>>(a, h->nsets);
     CK(cudaGetLastError());
@@ -1240,6 +1245,8 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
       CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, dev));
       const char* np = getenv("E2_NO_PIPE");
       h->no_pipe = np && np[0] == '1';
+      const char* npf = getenv("E2_NO_PREFETCH");
+      h->no_prefetch = npf && npf[0] == '1';
     }
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream_handle = h->stream;
