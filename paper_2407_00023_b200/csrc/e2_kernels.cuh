@@ -580,15 +580,26 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     return;
   }
   if ((threadIdx.x >> 5) == 1) {
+    // warp 1: LRU fixes + evictions of request i between barriers 2 and 1;
+    // its decision record between barriers 1 and 2 of the next request
+    // (beside warp 0's commit), when warp 0 writes the other scratch buffer
+    bool have = false;
+    i64 pli = 0;
+    Dec pdec;
+    const Scr* psb = nullptr;
     for (;;) {
       bar_pair(1);
+      if (have) replay_out(psb, a, pli, pdec);
       bar_pair(2);
       if (pp->stop) break;
       if (lane0()) g_ntouch = 0;
       wsync();
       const Scr* sb = pp->s;
+      pli = pp->li;
+      pdec = pp->dec;
+      psb = sb;
+      have = true;
       if (sb->fix_D > 0) path_lru_fix(sb, sb->fix_D, pp->g);
-      replay_out(sb, a, pp->li, pp->dec);
       replay_evict(a, pp->li, pp->g);
     }
     return;
