@@ -567,10 +567,8 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
             else break;
           }
           hi = idx;
-          PHASE_COUNT(18);
           continue;
         }
-        if (hint == hint2) PHASE_COUNT(19);
         fast = false;
         continue;
       }
@@ -583,7 +581,6 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
       }
       wsync();
       if (x != cur || nc == 0) {
-        PHASE_COUNT(20);
         fast = false;
         continue;
       }
@@ -611,7 +608,6 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
         const u32 okc = ballot(k < chunk && vp < hS);
         const int nvc = (okc == kFull) ? kWidth : ffs32(~okc);
         if (nvc == 0) {
-          PHASE_COUNT(21);
           fast = false;
           break;
         }

@@ -587,10 +587,14 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     i64 pli = 0;
     Dec pdec;
     const Scr* psb = nullptr;
+    PHASE_MARK1(23);
     for (;;) {
       bar_pair(1);
+      PHASE_MARK1(23);  // waiting
       if (have) replay_out(psb, a, pli, pdec);
+      PHASE_MARK1(22);  // decision record
       bar_pair(2);
+      PHASE_MARK1(23);
       if (pp->stop) break;
       if (lane0()) g_ntouch = 0;
       wsync();
@@ -600,7 +604,9 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       psb = sb;
       have = true;
       if (sb->fix_D > 0) path_lru_fix(sb, sb->fix_D, pp->g);
+      PHASE_MARK1(20);  // LRU fixes
       replay_evict(a, pp->li, pp->g);
+      PHASE_MARK1(21);  // evictions
     }
     return;
   }

@@ -84,8 +84,20 @@ E2_HD void touch(u32) {}
     }                                                          \
     wsync();                                                   \
   } while (0)
+// warp 1 of the pipelined replay: slots 20..23
+#define PHASE_MARK1(i)                                         \
+  do {                                                         \
+    wsync();                                                   \
+    const u64 _pn = clock64();                                 \
+    if (lane0()) {                                             \
+      HOT.phase_cycles[i] += _pn - HOT.phase_last1;            \
+      HOT.phase_last1 = _pn;                                   \
+    }                                                          \
+    wsync();                                                   \
+  } while (0)
 #elif defined(E2_PHASES)
 #include <x86intrin.h>
+#define PHASE_MARK1(i)
 #define PHASE_MARK(i)                                          \
   do {                                                         \
     const u64 _pn = __rdtsc();                                 \
@@ -94,6 +106,7 @@ E2_HD void touch(u32) {}
   } while (0)
 #else
 #define PHASE_MARK(i)
+#define PHASE_MARK1(i)
 #endif
 #if defined(E2_PHASES)
 #if E2_DEVICE_BUILD
