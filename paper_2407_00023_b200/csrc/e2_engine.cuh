@@ -1429,7 +1429,9 @@ E2_DNI void evict_tail(u32 v, i64 tok, int g) {
   const u64 id0 = r->id, la0 = dbits(rla(r)[g]), cm = r->cmask;
   const bool leaf = rleaf(r, v, g, G);
   // other instances where v is a leaf: split re-keys them (new suffix id)
+  PHASE_MARK1(28);
   const u32 q = split_node(v, (u32)(len - tok), false);
+  PHASE_MARK1(25);
   if (q == kNil) return;
   const u64 id1 = nget(v)->id;
   for (u64 m = cm & ~(1ull << g); m; m &= m - 1) {
@@ -1472,6 +1474,7 @@ E2_DNI void evict_lru(int g, i64 over) {
   }
   wsync();
   PHASE_MARK(11);
+  PHASE_MARK1(24);
   const u32 nv = (u32)DEV.scr_val[(u64)DEV.cfg.G * DEV.scap];
   for (u32 i = 0; i < nv && !HOT.err; ++i) {
     const u32 v = DEV.vic_slot[i];
@@ -1480,9 +1483,11 @@ E2_DNI void evict_lru(int g, i64 over) {
     if (tok < len) {
       PHASE_COUNT(13);
       evict_tail(v, tok, g);
+      PHASE_MARK1(26);
     } else {
       PHASE_COUNT(14);
       clear_cached(v, g);
+      PHASE_MARK1(27);
     }
   }
 }

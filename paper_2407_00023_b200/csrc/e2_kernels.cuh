@@ -153,7 +153,7 @@ E2_D i64 prune_dead() {
           HOT.node_count--;
         }
         wsync();
-        child_erase(par, ft);
+        child_erase_at(rv->ctpos, par, ft);
         NodeRec* rp = nget(par);
         if (lane0()) {
           rp->nchild -= 1;

@@ -289,6 +289,14 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32)
   }
 }
 
+__global__ void k_ct_reindex(const CtEntry* ct, u64 cap, char* rec, u32 rs) {
+  const u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cap) return;
+  const CtEntry e = ct[j];
+  if (e.key == kEmptyKey || e.key == kTombKey) return;
+  ((NodeRec*)(rec + (u64)e.val * rs))->ctpos = (u32)j;
+}
+
 __global__ void k_arena_index(i64 n, i64 base_tok, const i64* offsets, i64* off, i64* len, i64 first) {
   i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -460,6 +468,17 @@ void host_rehash_ct(e2_handle* h, u64 new_cap) {
   dfree(d.ct);
   d.ct = talloc<CtEntry>(new_cap);
   h2d(d.ct, nt.data(), new_cap * sizeof(CtEntry), h->stream);
+  // every node's record holds the position of its own entry (ctpos)
+#if E2_DEVICE_BUILD
+  k_ct_reindex<<<(unsigned)((new_cap + 255) / 256), 256, 0, h->stream>>>(d.ct, new_cap, d.rec, d.rs);
+  CK(cudaGetLastError());
+#else
+  for (u64 j = 0; j < new_cap; ++j) {
+    const u64 k = nt[j].key;
+    if (k == kEmptyKey || k == kTombKey) continue;
+    ((NodeRec*)(d.rec + (u64)nt[j].val * d.rs))->ctpos = (u32)j;
+  }
+#endif
   ssync(h->stream);
   d.ct_mask = mask;
 }
@@ -1865,7 +1884,7 @@ int e2_profile_reset(e2_handle* h, int32_t enable_timing) {
 extern "C" int e2_debug_phases(e2_handle* h, uint64_t* out) {
   return guard(h, [&] {
     pull_hot(h);
-    for (int i = 0; i < 24; ++i) out[i] = h->hot.phase_cycles[i];
+    for (int i = 0; i < 32; ++i) out[i] = h->hot.phase_cycles[i];
   });
 }
 #endif

@@ -37,7 +37,7 @@ struct NodeRec {
   u64 cmask;      // bit g: cached on instance g
   u64 lamask;     // bit g: last_access[g] entry exists
   i32 nchild;
-  i32 pad0;
+  u32 ctpos;  // position of this node's own child-table entry (its parent's key for it)
   u64 pad1;
   // followed by: double la[G]; i32 hits[G]; i32 ccc[G];
 };
@@ -176,7 +176,7 @@ struct Hot {
   i32 err, why;
   i64 err_req;  // request index / op index that failed
   i64 done;     // ops fully processed in the last launch
-  u64 phase_cycles[24];  // E2_PHASES builds: clock64 per replay phase
+  u64 phase_cycles[32];  // E2_PHASES builds: clock64 per replay phase
   u64 phase_last, phase_last1;
 };
 static_assert(sizeof(Hot) % 8 == 0, "Hot is copied as u64 words");

@@ -265,6 +265,10 @@ E2_D void nflush() {
 
 #endif
 
+// single-lane record access inside a lane-0 block (no cache fill): the
+// cached copy if resident, else HBM.
+E2_HD NodeRec* nget_lane(u32 s) { return npoke(s); }
+
 // ---------------------------------------------------------------------------
 // Child table: open addressing, linear probing, key = parent<<32 | token.
 // Replaces TreeNode::children (std::map) lookups, prefix_tree.cpp:85, 160.
@@ -317,7 +321,8 @@ E2_D u32 child_lookup(u32 parent, i32 tok) {
   return p.found ? p.val : kNil;
 }
 
-// warp-wide; key must be absent.
+// warp-wide; key must be absent.  Records the entry's position in the
+// child's record (ctpos), so re-pointing or erasing it needs no probe.
 E2_DNI bool child_insert(u32 parent, i32 tok, u32 child) {
   const u64 key = ckey(parent, tok);
   Probe p = ct_probe(key);
@@ -333,6 +338,8 @@ E2_DNI bool child_insert(u32 parent, i32 tok, u32 child) {
     e.val = child;
     e.pad = 0;
     DEV.ct[p.pos] = e;
+    NodeRec* rc = nget_lane(child);
+    rc->ctpos = (u32)p.pos;
   }
   wsync();
   return true;
@@ -363,6 +370,19 @@ E2_DNI void child_erase(u32 parent, i32 tok) {
   }
   wsync();
 }
+
+// warp-wide: erase the entry at a known position (the node's ctpos);
+// falls back to a probe if the position does not hold the key.
+E2_DNI void child_erase_at(u32 pos, u32 parent, i32 tok) {
+  const u64 key = ckey(parent, tok);
+  if ((u64)pos <= DEV.ct_mask && DEV.ct[pos].key == key) {
+    if (lane0()) DEV.ct[pos].key = kTombKey;
+    wsync();
+    return;
+  }
+  child_erase(parent, tok);
+}
+
 
 // ---------------------------------------------------------------------------
 // Per-instance LRU index: ordered set of (last_access bits, id) over LRU
@@ -797,7 +817,10 @@ E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
     HOT.node_count++;
   }
   wsync();
-  child_update(hs.parent, hs.first_tok, q);
+  // the parent's entry for this edge now leads to the prefix (which copied
+  // the record, ctpos included); the suffix hangs under the prefix
+  if (lane0()) DEV.ct[hs.ctpos].val = q;
+  wsync();
   child_insert(q, tok_k, s);
   if (!rekey) return q;
   // LRU: the suffix inherits the leaf role under its new id.
