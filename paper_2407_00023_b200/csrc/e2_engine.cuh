@@ -1220,8 +1220,10 @@ E2_DNI u64 path_update(u32 tail, int g, double now, bool mark) {
 // commit (global_scheduler.cpp:160-175), optionally fused with the
 // driver's note_prefill_cached (see path_update).  Warp-wide.  Returns the
 // tail slot.
+// defer_inflight: the inflight sums and record are left to the caller
+// (the pipelined replay's second warp, inflight_insert).
 E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
-                  double now, bool mark, Scr* s_path, bool defer_lru = false) {
+                  double now, bool mark, Scr* s_path, bool defer_lru = false, bool defer_inflight = false) {
   if (s_path && lane0()) {
     s_path->fix_D = 0;
     s_path->cpath = -1;
@@ -1272,6 +1274,11 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
   } else {
     root_id = path_update(tail, g, now, mark);
   }
+  if (defer_inflight) {
+    if (lane0()) win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail, plen);
+    wsync();
+    return tail;
+  }
   if (lane0()) {
     win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail, plen);
     HOT.inflight_cached[g] += r.cached_len;
@@ -1299,6 +1306,37 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
   }
   wsync();
   return tail;
+}
+
+// The inflight half of commit (global_scheduler.cpp:172-174): sums and the
+// id -> placement record.  root_id is the first-level node of the committed
+// path.  Warp-wide (single-lane work).
+E2_DNI void inflight_insert(i64 req_id, int g, i64 cached_len, i64 n, double arrival, u64 root_id) {
+  if (lane0()) {
+    HOT.inflight_cached[g] += cached_len;
+    HOT.inflight_prompt[g] += n;
+    bool found;
+    const u64 i = inf_find(req_id, found);
+    if (i == ~0ull) {
+      set_err(kErrCapacity, kWhyInflightCap);
+    } else {
+      if (!found) {
+        HOT.inflight_n++;
+        if ((u64)HOT.inflight_n * 2 > DEV.inf_mask + 1) set_err(kErrCapacity, kWhyInflightCap);
+      }
+      InfRec e;
+      e.key = req_id;
+      e.gpu = g;
+      e.pad = 0;
+      e.cached = cached_len;
+      e.prompt = n;
+      e.arr = arrival;
+      e.root = root_id;
+      e.pad2 = 0;
+      DEV.inf[i] = e;
+    }
+  }
+  wsync();
 }
 
 // Stats (global_scheduler.cpp:183-189).

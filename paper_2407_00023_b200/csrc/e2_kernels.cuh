@@ -371,7 +371,7 @@ E2_D double replay_pre(Scr* s, const SerialArgs& a, i64 li) {
 // spec_w: a speculative decide of this request already validated by the
 // pipeline (its Walk and Scr path are current), or null.
 E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec, const Walk* spec_w = nullptr,
-                      bool defer_lru = false) {
+                      bool defer_lru = false, bool defer_inflight = false) {
   const i64 r = a.base + li;
   const i64 off = a.off[r], n = a.len[r];
   const i32* seq = DEV.tok + off;
@@ -385,7 +385,7 @@ E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec,
   if (!dec.ok) return false;
   PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
-  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s, defer_lru);
+  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s, defer_lru, defer_inflight);
   if (HOT.err) return false;
   PHASE(2);
   if (lane0()) DEV.req_tail[r] = tail;
@@ -478,6 +478,13 @@ struct Pipe {
   i32 stop;
   Dec dec;
   Scr* s;  // the request's scratch (path, costs): double-buffered by warp 0
+  // request being committed: its inflight record + note_finished of its step
+  // are applied by warp 1 once warp 0 raises `ready` (= request index + 1)
+  volatile long long ready;
+  i64 c_id, c_cached, c_n;
+  u64 c_root;
+  double c_arr, c_now;
+  i32 c_g, c_defer;
 };
 
 E2_D void bar_pair(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
@@ -588,11 +595,19 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     Dec pdec;
     const Scr* psb = nullptr;
     PHASE_MARK1(23);
-    for (;;) {
+    for (i64 ci = 0;; ++ci) {
       bar_pair(1);
       PHASE_MARK1(23);  // waiting
       if (have) replay_out(psb, a, pli, pdec);
       PHASE_MARK1(22);  // decision record
+      // the request warp 0 is committing: its inflight record, then
+      // note_finished of its step (both before the next redirect upkeep)
+      while (pp->ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
+      if (pp->ready == ci + 1) {
+        if (pp->c_defer) inflight_insert(pp->c_id, pp->c_g, pp->c_cached, pp->c_n, pp->c_arr, pp->c_root);
+        replay_finish(a, ci, pp->c_now);
+      }
+      PHASE_MARK1(19);
       bar_pair(2);
       PHASE_MARK1(23);
       if (pp->stop) break;
@@ -634,13 +649,49 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       break;
     }
     bool ok;
-    if (specd && !s->spec_bad && !spec_conflict(s)) {
+    bool valid = specd && !s->spec_bad && !spec_conflict(s);
+    if (valid) {
       if (DEV.cfg.mode == 0 && lane0()) HOT.stats[kStTreeReads]++;
       wsync();
-      ok = replay_main(s, a, i, now, dec, &w, true);
     } else {
       PHASE_COUNT(17);  // speculation redone
-      ok = replay_main(s, a, i, now, dec, nullptr, true);
+      const i64 r = a.base + i;
+      dec = decide(s, DEV.tok + a.off[r], a.len[r], a.L[i], a.hint + i * a.hstride, a.hstride, a.S[i], now, w, false,
+                   a.lead ? a.lead + i : nullptr, a.hint);
+    }
+    // hand the inflight record (prefix root known before the insert: the
+    // first matched level keeps its id through a split at L; with nothing
+    // matched it is the new leaf, id next_id) and this step's note_finished
+    // to warp 1, which applies them beside this warp's tree insert
+    {
+      const i64 r = a.base + i;
+      const i64 L = a.L[i];
+      const bool defer = dec.ok && DEV.cfg.mode == 0 && a.len[r] > 0 && s->npath >= 0 && (L == 0 || s->npath > 0);
+      u64 root = 0;
+      if (defer) root = L > 0 ? nget(PSLOT(s, 0))->id : HOT.next_id;
+      if (dec.ok && lane0()) {
+        pp->c_id = a.ids[r];
+        pp->c_g = dec.gpu;
+        pp->c_cached = dec.cached_len;
+        pp->c_n = a.len[r];
+        pp->c_arr = a.arr[r];
+        pp->c_root = root;
+        pp->c_now = now;
+        pp->c_defer = defer ? 1 : 0;
+        __threadfence_block();
+        if (defer) pp->ready = i + 1;
+      }
+      wsync();
+      ok = dec.ok && replay_main(s, a, i, now, dec, &w, true, defer);
+      // not deferred (round robin, very deep paths): the commit wrote the
+      // inflight record itself; only then may warp 1 apply note_finished
+      if (dec.ok && !defer) {
+        if (lane0()) {
+          __threadfence_block();
+          pp->ready = i + 1;
+        }
+        wsync();
+      }
     }
     if (!ok || HOT.err) {
       fail = i;
@@ -656,11 +707,6 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     wsync();
     bar_pair(2);
     past1 = false;
-    replay_finish(a, i, now);
-    if (HOT.err) {
-      fail = i;
-      break;
-    }
   }
   if (!past1) bar_pair(1);  // wait for the last evict
   if (HOT.err && fail < 0) fail = a.n - 1;  // the last evict failed

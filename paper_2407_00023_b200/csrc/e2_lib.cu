@@ -157,6 +157,8 @@ __global__ void __launch_bounds__(96, 1) k_serial(SerialArgs a, u32 nsets) {
   if (threadIdx.x == 0) {
     g_pf_cur = -1;
     g_pf_stop = 0;
+    pipe.ready = 0;
+    pipe.stop = 0;
   }
   __syncthreads();
   serial_body(ss, a, blockDim.x >= 64 ? &pipe : nullptr);
