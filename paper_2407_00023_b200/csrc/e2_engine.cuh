@@ -26,6 +26,9 @@ struct Scr {
   i32 spec_bad;  // a speculative decide gave up (see decide)
   i32 fix_D;     // path levels whose LRU fixes path_update_par deferred (0: none)
   i32 cpath;     // levels of the committed path in pslot (-1: not recorded)
+  i32 win_done;  // the scheduled-window entry was appended before the commit (pipelined replay)
+  u64 widx;      // its ring position: commit fills in the tail slot and path-log length
+  double pre_now;  // this request's `now`, computed by replay_pre on the other warp
   i32 npath;  // levels recorded by walk_par (-1: path too deep, sequential fallback)
   // the request's root path, top-down (walk_par / commit)
   u32 pslot[kMaxPath + 1];
@@ -1224,9 +1227,11 @@ E2_DNI u64 path_update(u32 tail, int g, double now, bool mark) {
 // (the pipelined replay's second warp, inflight_insert).
 E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
                   double now, bool mark, Scr* s_path, bool defer_lru = false, bool defer_inflight = false) {
+  const bool win_done = s_path && s_path->win_done;
   if (s_path && lane0()) {
     s_path->fix_D = 0;
     s_path->cpath = -1;
+    s_path->win_done = 0;
   }
   wsync();
   if (DEV.cfg.mode == 1) {
@@ -1275,7 +1280,16 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
     root_id = path_update(tail, g, now, mark);
   }
   if (defer_inflight) {
-    if (lane0()) win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail, plen);
+    if (lane0()) {
+      if (win_done) {
+        // appended early (window_early): hit expiry reads these two fields
+        WinEnt* e = &DEV.win[wslot(g, s_path->widx)];
+        e->slot = tail;
+        e->plen = plen;
+      } else {
+        win_add_sched(g, now, r.moc, DEV.cfg.default_out, tail, plen);
+      }
+    }
     wsync();
     return tail;
   }

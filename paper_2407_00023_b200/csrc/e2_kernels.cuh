@@ -606,6 +606,14 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       if (pp->ready == ci + 1) {
         if (pp->c_defer) inflight_insert(pp->c_id, pp->c_g, pp->c_cached, pp->c_n, pp->c_arr, pp->c_root);
         replay_finish(a, ci, pp->c_now);
+        // the next request's `now` and redirect upkeep: its windows are final
+        // (this step's scheduled entry was appended before `ready`)
+        if (pp->c_defer && ci + 1 < a.n) {
+          Scr* sn = s2 + ((ci + 1) & 1);
+          const double nn = replay_pre(sn, a, ci + 1);
+          if (lane0()) sn->pre_now = nn;
+          wsync();
+        }
       }
       PHASE_MARK1(19);
       bar_pair(2);
@@ -627,10 +635,11 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
   }
   i64 i = 0, fail = -1;
   bool past1 = false;  // warp 0 is between barrier 1 and barrier 2
+  bool pre_done = false;  // warp 1 ran this request's replay_pre
   for (; i < a.n; ++i) {
     Scr* s = s2 + (i & 1);  // warp 1 reads the other buffer (request i-1) meanwhile
     if (lane0()) g_pf_cur = i;
-    const double now = replay_pre(s, a, i);
+    const double now = pre_done ? s->pre_now : replay_pre(s, a, i);
     // decide speculatively while warp 1 evicts for request i-1
     Dec dec;
     Walk w;
@@ -678,10 +687,19 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
         pp->c_root = root;
         pp->c_now = now;
         pp->c_defer = defer ? 1 : 0;
+        if (defer) {
+          // the scheduled-window entry first: warp 1's redirect upkeep of
+          // the next request reads the windows (commit fills in its slot
+          // and path-log length)
+          s->widx = HOT.ws_tail[dec.gpu];
+          win_add_sched(dec.gpu, now, dec.moc, DEV.cfg.default_out, kNil, kNil);
+          s->win_done = 1;
+        }
         __threadfence_block();
         if (defer) pp->ready = i + 1;
       }
       wsync();
+      pre_done = defer && i + 1 < a.n;
       ok = dec.ok && replay_main(s, a, i, now, dec, &w, true, defer);
       // not deferred (round robin, very deep paths): the commit wrote the
       // inflight record itself; only then may warp 1 apply note_finished
