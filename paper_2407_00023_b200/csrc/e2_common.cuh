@@ -123,6 +123,13 @@ inline double i2d(i64 v) { return (double)v; }
 #endif
 
 E2_HD bool lane0() { return lane() == 0; }
+
+// L1 prefetch of a global address (no-op in the host emulation)
+#if E2_DEVICE_BUILD
+E2_D void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+#else
+inline void pf(const void*) {}
+#endif
 #if E2_DEVICE_BUILD
 E2_D bool thread0() { return threadIdx.x == 0; }  // lane 0 of warp 0
 #else

@@ -1513,11 +1513,13 @@ E2_DNI void evict_tail(u32 v, i64 tok, int g) {
 E2_DNI void evict_lru(int g, i64 over) {
   if (lane0()) {
     u32 nv = 0;
-    plan_eviction(g, over, true, [&](u32 v, i64 tok, const NodeRec*) {
+    plan_eviction(g, over, true, [&](u32 v, i64 tok, const NodeRec* rv) {
       if (nv < DEV.vcap) {
         DEV.vic_slot[nv] = v;
         DEV.vic_tok[nv] = tok;
         nv++;
+        // a partial victim is split at len - tok: fetch that token early
+        if (tok < (i64)rv->edge_len) pf(DEV.tok + rv->edge_off + (rv->edge_len - tok));
       } else {
         set_err(kErrCapacity, kWhyScratchCap);
       }

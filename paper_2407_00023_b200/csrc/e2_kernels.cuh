@@ -513,7 +513,6 @@ E2_D bool spec_conflict(const Scr* s) {
 __shared__ volatile long long g_pf_cur;
 __shared__ volatile int g_pf_stop;
 
-E2_D void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 E2_D void prefetch_request(const SerialArgs& a, i64 j) {
   const int G = DEV.cfg.G;

@@ -794,7 +794,11 @@ E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
   const u64 new_id = HOT.next_id;
   const i32 tok_k = DEV.tok[hs.edge_off + k];
   // prefix: copy the whole record (la/hits), then fix header and ccc
+#if defined(E2_SMEM_NODECACHE)
   NodeRec* rq = nnew(q);
+#else
+  NodeRec* rq = grec(q);  // every word is overwritten by the copy below
+#endif
   rs = nget(s);
   {
     const u64* src = (const u64*)rs;
