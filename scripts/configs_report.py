@@ -37,6 +37,7 @@ def main(names):
         cpu = time.perf_counter() - t0
         bb = type(b)(b.decisions[:trr.n], b.costs[:trr.n], None, min(b.n_done, trr.n))
         d = diff_decisions(a, bb)
+        nodes = s.node_count()
         # the product on exactly the reference's prefix (same work on both sides)
         same = None
         if trr.n < tr.n:
@@ -54,7 +55,7 @@ def main(names):
             "reference_requests": trr.n, "reference_decisions_per_s": trr.n / cpu,
             "b200_decisions_per_s_on_reference_prefix": same if same is not None else tr.n / (kms / 1000),
             "bit_exact_on_reference_prefix": d is None, "first_mismatch": d,
-            "nodes": s.node_count(),
+            "nodes": nodes,
         }), flush=True)
         s.close(); r.close()
 
