@@ -1489,11 +1489,7 @@ E2_DNI void evict_tail(u32 v, i64 tok, int g) {
   for (u64 m = cm & ~(1ull << g); m; m &= m - 1) {
     const int o = ffs64(m);
     const NodeRec* rv = nget(v);
-    if (rccc(rv, G)[o] == 0) {
-      const u64 l = dbits(rla(rv)[o]);
-      lru_erase(o, l, id0);
-      lru_insert(o, l, id1, v);
-    }
+    if (rccc(rv, G)[o] == 0) lru_rekey(o, dbits(rla(rv)[o]), id0, id1, v);
   }
   // clear the suffix on g without touching g's index, then relabel
   r = nget(v);

@@ -751,6 +751,55 @@ E2_DNI void lru_relabel(int g, u64 kla, u64 kid, u32 slot) {
   wsync();
 }
 
+// warp-wide: the entry (kla, old_id) is re-keyed to (kla, new_id), new_id
+// larger than every id in the index (split suffixes take next_id).  When no
+// key lies between the two (the usual case: no other leaf shares this
+// last_access), the entry keeps its position and only its id and slot
+// change; otherwise it is erased and re-inserted.  Same set either way.
+E2_DNI void lru_rekey(int g, u64 kla, u64 old_id, u64 new_id, u32 slot) {
+  const u32 n = HOT.dir_n[g];
+  u32 k;
+  const DirEntry h0 = DEV.dir[dring(g, 0)];
+  if (n > 0 && !kless(h0.max_la, h0.max_id, kla, old_id))
+    k = 0;
+  else
+    k = dir_lower_bound(g, kla, old_id);
+  if (k >= n) {
+    if (lane0()) set_err(kErrSim, kWhyWalk);
+    wsync();
+    return;
+  }
+  const DirEntry e = k == 0 ? h0 : DEV.dir[dring(g, k)];
+  const u64 base = (u64)e.page * kPage;
+  const u32 m = vote(e.cnt, [&](int j) { return DEV.pg_la[base + j] == kla && DEV.pg_id[base + j] == old_id; });
+  wsync();
+  if (!m) {
+    if (lane0()) set_err(kErrSim, kWhyWalk);
+    wsync();
+    return;
+  }
+  const int idx = ffs32(m);
+  bool inplace = true;
+  if (idx + 1 < e.cnt) {
+    inplace = kless(kla, new_id, DEV.pg_la[base + idx + 1], DEV.pg_id[base + idx + 1]);
+  } else if (k + 1 < n) {
+    const DirEntry e2 = DEV.dir[dring(g, k + 1)];
+    const u64 b2 = (u64)e2.page * kPage;
+    inplace = kless(kla, new_id, DEV.pg_la[b2], DEV.pg_id[b2]);
+  }
+  if (!inplace) {
+    lru_erase(g, kla, old_id);
+    lru_insert(g, kla, new_id, slot);
+    return;
+  }
+  if (lane0()) {
+    DEV.pg_id[base + idx] = new_id;
+    DEV.pg_slot[base + idx] = slot;
+    if (idx == e.cnt - 1) DEV.dir[dring(g, k)].max_id = new_id;
+  }
+  wsync();
+}
+
 // ---------------------------------------------------------------------------
 // Node state helpers (all warp-wide; records via the node cache)
 // ---------------------------------------------------------------------------
@@ -833,11 +882,7 @@ E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
     const int g = ffs64(m);
     m &= m - 1;
     const NodeRec* r = nget(s);
-    if (rccc(r, G)[g] == 0) {
-      const u64 l = dbits(rla(r)[g]);
-      lru_erase(g, l, hs.id);
-      lru_insert(g, l, new_id, s);
-    }
+    if (rccc(r, G)[g] == 0) lru_rekey(g, dbits(rla(r)[g]), hs.id, new_id, s);
   }
   return q;
 }
