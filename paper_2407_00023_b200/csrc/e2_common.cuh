@@ -19,7 +19,15 @@
 #define E2_HD __device__ __forceinline__
 #define E2_HDX __host__ __device__ __forceinline__
 #define E2_D __device__ __forceinline__
+// Every engine function is inlined into the serial kernel: measured on C2,
+// device calls (ABI register save/restore, no optimisation across the call)
+// cost ~35% of the per-request time (99.6k vs 73.1k decisions/s with only
+// decide inlined).  -DE2_NOINLINE keeps the call structure (profiling).
+#if defined(E2_NOINLINE)
 #define E2_DNI __device__ __noinline__
+#else
+#define E2_DNI __device__ __forceinline__
+#endif
 #else
 #define E2_DEVICE_BUILD 0
 #define E2_HD inline

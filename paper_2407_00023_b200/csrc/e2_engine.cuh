@@ -961,7 +961,7 @@ E2_D bool any_need(const Scr* s, u64 set, i64 n) {
 // eviction term, the cost of instance g depends on the eviction only through
 // need = missed - (cap - cached_tokens[g]) <= 0, which an eviction (cached
 // tokens only decrease) cannot turn positive.
-E2_DNI Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, i64 hS, double now, Walk& w,
+E2_D Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, i64 hS, double now, Walk& w,
                   bool spec = false, const i64* lead = nullptr, const u32* hint_rows = nullptr) {
   Dec r;
   r.branch = 1;
