@@ -543,36 +543,60 @@ E2_D void prefetch_request(const SerialArgs& a, i64 j) {
     pf(&DEV.inf[h]);
     pf(&DEV.inf[(h + 2) & DEV.inf_mask]);
   }
+  if (lane() == 6 && a.lead) {
+    const i64 ld = a.lead[j];  // in-batch leader: its committed path row
+    if (ld >= 0) pf(a.hint + ld * a.hstride);
+  }
   for (int g = lane(); g < G; g += kWidth) {
     pf(&DEV.win[wslot(g, HOT.ws_head[g])]);
+    pf(&DEV.comp[wslot(g, HOT.wc_head[g])]);
     if (HOT.dir_n[g] > 0) {
       const DirEntry e = DEV.dir[dring(g, 0)];
       if (e.page < DEV.page_cap) {
         const u64 pi = (u64)e.page * kPage;
         pf(&DEV.pg_la[pi]);
+        pf(&DEV.pg_la[pi + 16]);
         pf(&DEV.pg_id[pi]);
-        const u32 v = DEV.pg_slot[pi];
-        if (v < DEV.node_cap) {
-          const char* rec = (const char*)grec(v);
-          pf(rec);
-          pf(rec + 128);
-          const NodeRec* rv = (const NodeRec*)rec;
-          const u32 p = rv->parent;
-          if (p < DEV.node_cap) pf(grec(p));
+        pf(&DEV.pg_id[pi + 16]);
+        // the first two LRU victims and their parents
+        for (int q = 0; q < 2 && q < e.cnt; ++q) {
+          const u32 v = DEV.pg_slot[pi + q];
+          if (v < DEV.node_cap) {
+            const char* rec = (const char*)grec(v);
+            pf(rec);
+            pf(rec + 128);
+            const NodeRec* rv = (const NodeRec*)rec;
+            const u32 p = rv->parent;
+            if (p < DEV.node_cap) pf(grec(p));
+          }
         }
       }
-      pf(&DEV.dir[dring(g, HOT.dir_n[g] - 1)]);
+      const DirEntry t = DEV.dir[dring(g, HOT.dir_n[g] - 1)];
+      if (t.page < DEV.page_cap && t.cnt < kPage) {
+        const u64 ti = (u64)t.page * kPage + t.cnt;  // where the next fresh key lands
+        pf(&DEV.pg_la[ti]);
+        pf(&DEV.pg_id[ti]);
+        pf(&DEV.pg_slot[ti]);
+      }
     }
   }
 }
+
+#ifndef E2_PF_SLEEP
+#define E2_PF_SLEEP 4000  // ns between polls of warp 0's progress
+#endif
+#ifndef E2_PF_AHEAD
+#define E2_PF_AHEAD 2
+#endif
+constexpr int kPfAhead = E2_PF_AHEAD;  // requests prefetched ahead of warp 0
 
 E2_D void prefetch_loop(const SerialArgs& a) {
   i64 done = -1;
   while (!g_pf_stop) {
     const i64 cur = g_pf_cur;
-    const i64 want = min_<i64>(cur + 1, a.n - 1);
+    const i64 want = min_<i64>(cur + kPfAhead, a.n - 1);
     if (done >= want) {
-      __nanosleep(256);
+      __nanosleep(E2_PF_SLEEP);
       continue;
     }
     done = max_<i64>(done + 1, cur + 1);
