@@ -626,6 +626,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       // the request warp 0 is committing: its inflight record, then
       // note_finished of its step (both before the next redirect upkeep)
       while (pp->ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
+      PHASE_MARK1(29);  // waiting for warp 0's hand-off
       if (pp->ready == ci + 1) {
         if (pp->c_defer) inflight_insert(pp->c_id, pp->c_g, pp->c_cached, pp->c_n, pp->c_arr, pp->c_root);
         replay_finish(a, ci, pp->c_now);

@@ -16,6 +16,6 @@ names = ["redirects", "decide_other", "commit_other", "decision_out", "evict_app
          "cost_pick", "ensure_path", "path_update", "evict_plan", "", "", "", ""]
 tot = sum(buf[:12]) + buf[16]
 print(name, n, "cycles/request total %.0f" % (tot / n), " ".join("%s=%.0f" % (names[i], buf[i] / n) for i in range(16) if names[i]), "wait_evict=%.0f" % (buf[16] / n), "spec_redo=%.3f" % (buf[17] / n),
-      "| warp1: fixes=%.0f evict=%.0f out=%.0f wait=%.0f" % tuple(buf[k] / n for k in (20, 21, 22, 23)),
+      "| warp1: fixes=%.0f evict=%.0f out=%.0f spin=%.0f books=%.0f" % tuple(buf[k] / n for k in (20, 21, 22, 29, 19)),
       "| evict: plan=%.0f tail_pre=%.0f split=%.0f tail_post=%.0f whole=%.0f" % tuple(buf[k] / n for k in (24, 28, 25, 26, 27)),
       "| per request: walk_fallback_probes=%.3f evict_tail=%.3f evict_whole=%.3f" % (buf[12] / n, buf[13] / n, buf[14] / n))
