@@ -63,3 +63,26 @@ def test_replay_error_hostsim(hostsim_lib, ref_lib, gen_lib, n, k, batch):
 def test_replay_error_b200(b200_lib, ref_lib, gen_lib, n, k, batch):
     cfg, tr = _case(gen_lib, n, k, batch)
     _check(b200_lib, ref_lib, cfg, tr, k)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 33])
+def test_tiny_replays_hostsim(hostsim_lib, ref_lib, gen_lib, n):
+    cfg = dataclasses.replace(W.CONFIGS["c1"], n_requests=n)
+    tr = cfg.trace(lib=gen_lib)
+    _, a = replay(ref_lib, cfg, tr)
+    _, b = replay(hostsim_lib, cfg, tr)
+    assert a.n_done == b.n_done == n
+    assert diff_decisions(a, b) is None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 2, 3, 33, 2049])
+def test_tiny_replays_b200(b200_lib, ref_lib, gen_lib, n):
+    """Pipeline start-up and drain with fewer requests than pipeline stages
+    (and one request past the first ramp batch)."""
+    cfg = dataclasses.replace(W.CONFIGS["c1"], n_requests=n)
+    tr = cfg.trace(lib=gen_lib)
+    _, a = replay(ref_lib, cfg, tr)
+    _, b = replay(b200_lib, cfg, tr)
+    assert a.n_done == b.n_done == n
+    assert diff_decisions(a, b) is None
