@@ -214,7 +214,20 @@ E2_D void subtree_apply(u32 root, int g, double now, bool mark) {
   }
 }
 
-E2_D void api_op(Scr* s, const OpDesc& op, const u32* hint, int nh, ApiOut* out) {
+// dL: the matched length K1 left on the device (used when op.L < 0, so a
+// per-call API op needs no host round trip between the match and the op).
+// op.L == kMatchInline: match the sequence here first (one warp, K1's
+// match_one with its path hints), so a per-call op is a single launch.
+constexpr i64 kMatchInline = -2;
+E2_D void api_op(Scr* s, const OpDesc& op0, const u32* hint, int nh, ApiOut* out, const i64* dL = nullptr) {
+  OpDesc op = op0;
+  if (op.L == kMatchInline) {
+    const MatchRes m = match_one(DEV.tok + op.off, op.len, (u32*)hint, nh);
+    op.L = m.S;
+    wsync();
+  } else if (op.L < 0) {
+    op.L = dL ? dL[0] : 0;
+  }
   const int G = DEV.cfg.G;
   if (lane0()) s->loads_ok = 0;
   wsync();
@@ -779,7 +792,7 @@ E2_D void serial_body(Scr* s, const SerialArgs& a, void* pipe = nullptr) {
 #endif
     replay_seq(s, a);
   } else {
-    api_op(s, a.op, a.hint, a.hstride, a.out);
+    api_op(s, a.op, a.hint, a.hstride, a.out, a.L);
     if (lane0()) HOT.done = HOT.err ? 0 : 1;
     wsync();
   }

@@ -344,6 +344,11 @@ struct e2_handle {
   u32* g_tv = nullptr;
   u64 g_mask = 0;
   int n_sm = 148;
+  Hot dev_hot;  // the hot state last pushed to / pulled from the device
+  bool dev_hot_valid = false;
+  // pinned host staging for the per-call API: [Hot][ApiOut][off, len][tokens]
+  char* pin = nullptr;
+  size_t pin_cap = 0;
   bool no_pipe = false;      // E2_NO_PIPE=1: single-warp replays (dev comparisons)
   bool no_prefetch = false;  // E2_NO_PREFETCH=1: no prefetch warp (dev comparisons)
   unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions, [2] deepest K1 path beyond the hint stride
@@ -428,16 +433,33 @@ void prof_flush(e2_handle*) {}
 // The kernels read the handle's pointers/config from constant memory.
 void upload_dev(e2_handle* h) {
 #if E2_DEVICE_BUILD
+  // skipped when the constant bank already holds this descriptor (calls are
+  // serialised across handles, and each call completes before returning)
+  static Dev last;
+  static bool last_valid = false;
+  if (last_valid && memcmp(&last, &h->d, sizeof(Dev)) == 0) return;
   CK(cudaMemcpyToSymbolAsync(g_dev, &h->d, sizeof(Dev), 0, cudaMemcpyHostToDevice, h->stream));
+  last = h->d;
+  last_valid = true;
 #else
   g_dev_h = h->d;
 #endif
 }
 
-void push_hot(e2_handle* h) { h2d(h->d.hot_g, &h->hot, sizeof(Hot), h->stream); }
+// The host mirror of the hot state is pushed only when it differs from the
+// last state known to be on the device (a per-call API op would otherwise
+// upload ~7 KB per call for nothing).
+void push_hot(e2_handle* h) {
+  if (h->dev_hot_valid && memcmp(&h->hot, &h->dev_hot, sizeof(Hot)) == 0) return;
+  h2d(h->d.hot_g, &h->hot, sizeof(Hot), h->stream);
+  h->dev_hot = h->hot;
+  h->dev_hot_valid = true;
+}
 void pull_hot(e2_handle* h) {
   d2h(&h->hot, h->d.hot_g, sizeof(Hot), h->stream);
   ssync(h->stream);
+  h->dev_hot = h->hot;
+  h->dev_hot_valid = true;
 }
 
 void zero_ptrs(Dev& d) {
@@ -901,30 +923,52 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
 #endif
 }
 
-// Append sequences to the arena and index them at request slots [first, first+n).
-void append_host_seq(e2_handle* h, const i32* seq, i64 len, i64 slot) {
+// Per-call API staging (pinned host memory).
+constexpr size_t kPinHead = (sizeof(Hot) + sizeof(ApiOut) + 63) / 64 * 64;
+
+// Pinned staging for the per-call API (async copies; reused after the call's
+// synchronisation).
+char* pin_reserve(e2_handle* h, size_t bytes) {
+  const size_t need = kPinHead + 16 + bytes;
+  if (need > h->pin_cap) {
+    const size_t cap = std::max<size_t>(need, 2 * h->pin_cap + (1 << 16));
+#if E2_DEVICE_BUILD
+    if (h->pin) {
+      ssync(h->stream);  // no async copy may still read the old buffer
+      cudaFreeHost(h->pin);
+    }
+    CK(cudaMallocHost((void**)&h->pin, cap));
+#else
+    free(h->pin);
+    h->pin = (char*)malloc(cap);
+#endif
+    h->pin_cap = cap;
+  }
+  return h->pin;
+}
+
+// Append tokens only (per-call API: the serial kernel gets offset/length as
+// arguments).
+void append_host_tokens(e2_handle* h, const i32* seq, i64 len) {
   reserve_tokens(h, h->tok_len + len);
-  reserve_requests(h, slot + 1);
-  h2d(h->tok + h->tok_len, seq, (size_t)len * 4, h->stream);
-  i64 o = h->tok_len, l = len;
-  h2d(h->r_off + slot, &o, 8, h->stream);
-  h2d(h->r_len + slot, &l, 8, h->stream);
+  char* p = pin_reserve(h, (size_t)len * 4);
+  i32* t = (i32*)(p + kPinHead + 16);
+  memcpy(t, seq, (size_t)len * 4);
+  h2d(h->tok + h->tok_len, t, (size_t)len * 4, h->stream);
   h->tok_len += len;
 }
+
 
 // One API op on one sequence (or none): append, match, run.
 void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match) {
   reserve_for(h, 1, len);
   if (seq) {
-    append_host_seq(h, seq, len, 0);
+    append_host_tokens(h, seq, len);
     op.off = h->tok_len - len;
     op.len = len;
     if (need_match) {
-      launch_match(h, 0, 1);
-      i64 L = 0;
-      d2h(&L, h->b_L, 8, h->stream);
-      ssync(h->stream);
-      op.L = L;
+      reserve_batch(h, 1);
+      op.L = kMatchInline;  // the serial kernel matches the sequence itself
     }
   }
   SerialArgs a;
@@ -933,12 +977,19 @@ void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match) 
   a.op = op;
   a.out = h->d_api;
   a.hint = need_match ? h->b_path : nullptr;
+  a.L = nullptr;
   a.hstride = h->hstride;
   push_hot(h);
   launch_serial(h, a);
-  pull_hot(h);
-  d2h(&h->api, h->d_api, sizeof(ApiOut), h->stream);
+  // one synchronisation for the mirrored hot state and the op's result
+  char* p = pin_reserve(h, 0);
+  d2h(p, h->d.hot_g, sizeof(Hot), h->stream);
+  d2h(p + sizeof(Hot), h->d_api, sizeof(ApiOut), h->stream);
   ssync(h->stream);
+  memcpy(&h->hot, p, sizeof(Hot));
+  memcpy(&h->api, p + sizeof(Hot), sizeof(ApiOut));
+  h->dev_hot = h->hot;
+  h->dev_hot_valid = true;
   check_hot_error(h);
 }
 
@@ -1324,6 +1375,9 @@ void e2_destroy(e2_handle* h) {
   }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   if (h->own_stream) cudaStreamDestroy(h->own_stream_handle);
+  if (h->pin) cudaFreeHost(h->pin);
+#else
+  free(h->pin);
 #endif
   delete h;
 }

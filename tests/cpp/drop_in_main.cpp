@@ -3,6 +3,7 @@
 // reference, compiled from its sources) and once on the drop-in
 // kvsched::b200::GlobalScheduler (include/e2sched.hpp over the C ABI).
 // Every Decision field and cost double must match.  Exit 0 on success.
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <deque>
@@ -63,21 +64,31 @@ int main(int argc, char** argv) {
   kvsched::b200::GlobalScheduler dut(4, cfg, TimeModel{}, GlobalPolicy{});
   std::vector<std::deque<std::pair<const TokenSeq*, int64_t>>> ca(4), cb(4);
   SimTime now = 0;
+  double t_ref = 0, t_dut = 0;  // seconds spent in each side's calls
+  using clk = std::chrono::steady_clock;
   for (size_t i = 0; i < reqs.size(); ++i) {
     const Request& r = reqs[i];
     now = std::max(now, r.arrival_ms);
+    auto t0 = clk::now();
     const Decision a = ref.schedule_request(r, now);
+    auto t1 = clk::now();
     const Decision b = dut.schedule_request(r, now);
+    auto t2 = clk::now();
+    t_ref += std::chrono::duration<double>(t1 - t0).count();
+    t_dut += std::chrono::duration<double>(t2 - t1).count();
     if (!same(a, b)) {
       std::printf("MISMATCH at request %zu\n", i);
       return 1;
     }
+    t0 = clk::now();
     step(ref, ca, r, now, trunk, a);
+    if (i >= 2000) ref.note_finished(reqs[i - 2000].id, now, reqs[i - 2000].output_len);
+    t1 = clk::now();
     step(dut, cb, r, now, trunk, b);
-    if (i >= 2000) {
-      ref.note_finished(reqs[i - 2000].id, now, reqs[i - 2000].output_len);
-      dut.note_finished(reqs[i - 2000].id, now, reqs[i - 2000].output_len);
-    }
+    if (i >= 2000) dut.note_finished(reqs[i - 2000].id, now, reqs[i - 2000].output_len);
+    t2 = clk::now();
+    t_ref += std::chrono::duration<double>(t1 - t0).count();
+    t_dut += std::chrono::duration<double>(t2 - t1).count();
   }
   const GlobalStats sa = ref.stats(), sb = dut.stats();
   if (sa.exploit != sb.exploit || sa.explore != sb.explore || sa.redirected != sb.redirected ||
@@ -86,5 +97,6 @@ int main(int argc, char** argv) {
     return 1;
   }
   std::printf("drop-in OK: %lld decisions identical (%s backend)\n", (long long)n, e2_backend());
+  std::printf("per-call loop: reference %.0f requests/s, %s %.0f requests/s\n", n / t_ref, e2_backend(), n / t_dut);
   return 0;
 }
