@@ -51,7 +51,7 @@ struct ApiOut {
 struct SerialArgs {
   i32 kind;  // 0 replay batch, 1 api op
   i32 eviction, prefill;
-  i32 pad;
+  i32 no_prefetch;  // pipelined replay: warp 2 idles (dev comparisons)
   i64 base, n;
   const i64* off;
   const i64* len;
@@ -494,6 +494,7 @@ struct Pipe {
   // request being committed: its inflight record + note_finished of its step
   // are applied by warp 1 once warp 0 raises `ready` (= request index + 1)
   volatile long long ready;
+  volatile long long books_done;  // warp 3: bookkeeping of requests [0, books_done) applied
   i64 c_id, c_cached, c_n;
   u64 c_root;
   double c_arr, c_now;
@@ -617,9 +618,41 @@ E2_D void prefetch_loop(const SerialArgs& a) {
   }
 }
 
+// Warp 3 (bookkeeping): for each request warp 0 hands off (`ready`), its
+// inflight record, note_finished of its step, then the next request's `now`
+// and redirect upkeep; publishes `books_done`.  Touches only the load
+// windows, the inflight map/sums, redirects and the next request's scratch
+// loads — state no other warp writes meanwhile (warp 0 inserts into the
+// tree, warp 1 writes the decision record or evicts).
+E2_D void books_loop(Scr* s2, const SerialArgs& a, Pipe* pp) {
+  for (i64 ci = 0;; ++ci) {
+    while (pp->ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
+    if (pp->ready != ci + 1) break;
+    if (pp->c_defer) inflight_insert(pp->c_id, pp->c_g, pp->c_cached, pp->c_n, pp->c_arr, pp->c_root);
+    replay_finish(a, ci, pp->c_now);
+    // the next request's `now` and redirect upkeep: its windows are final
+    // (this step's scheduled entry was appended before `ready`)
+    if (pp->c_defer && ci + 1 < a.n) {
+      Scr* sn = s2 + ((ci + 1) & 1);
+      const double nn = replay_pre(sn, a, ci + 1);
+      if (lane0()) sn->pre_now = nn;
+      wsync();
+    }
+    if (lane0()) {
+      __threadfence_block();
+      pp->books_done = ci + 1;
+    }
+    wsync();
+  }
+}
+
 E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
   if ((threadIdx.x >> 5) == 2) {
-    prefetch_loop(a);
+    if (!a.no_prefetch) prefetch_loop(a);
+    return;
+  }
+  if ((threadIdx.x >> 5) == 3) {
+    books_loop(s2, a, pp);
     return;
   }
   if ((threadIdx.x >> 5) == 1) {
@@ -636,23 +669,6 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       PHASE_MARK1(23);  // waiting
       if (have) replay_out(psb, a, pli, pdec);
       PHASE_MARK1(22);  // decision record
-      // the request warp 0 is committing: its inflight record, then
-      // note_finished of its step (both before the next redirect upkeep)
-      while (pp->ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
-      PHASE_MARK1(29);  // waiting for warp 0's hand-off
-      if (pp->ready == ci + 1) {
-        if (pp->c_defer) inflight_insert(pp->c_id, pp->c_g, pp->c_cached, pp->c_n, pp->c_arr, pp->c_root);
-        replay_finish(a, ci, pp->c_now);
-        // the next request's `now` and redirect upkeep: its windows are final
-        // (this step's scheduled entry was appended before `ready`)
-        if (pp->c_defer && ci + 1 < a.n) {
-          Scr* sn = s2 + ((ci + 1) & 1);
-          const double nn = replay_pre(sn, a, ci + 1);
-          if (lane0()) sn->pre_now = nn;
-          wsync();
-        }
-      }
-      PHASE_MARK1(19);
       bar_pair(2);
       PHASE_MARK1(23);
       if (pp->stop) break;
@@ -676,6 +692,10 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
   for (; i < a.n; ++i) {
     Scr* s = s2 + (i & 1);  // warp 1 reads the other buffer (request i-1) meanwhile
     if (lane0()) g_pf_cur = i;
+    // warp 3 applied request i-1's bookkeeping (and, if deferred, prepared
+    // this request's `now` and loads)
+    if (i > 0)
+      while (pp->books_done < i) __nanosleep(32);
     const double now = pre_done ? s->pre_now : replay_pre(s, a, i);
     // decide speculatively while warp 1 evicts for request i-1
     Dec dec;

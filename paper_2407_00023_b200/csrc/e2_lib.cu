@@ -130,7 +130,7 @@ constexpr size_t kScrBytes = (2 * sizeof(Scr) + 127) / 128 * 128;
 // two-warp pipeline of e2_kernels.cuh (warp 1 runs the evictions).
 // Dynamic shared memory: two Scr buffers (the pipeline alternates them per
 // request), then the node-cache arrays (a stub unless E2_SMEM_NODECACHE).
-__global__ void __launch_bounds__(96, 1) k_serial(SerialArgs a, u32 nsets) {
+__global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
   __shared__ Pipe pipe;
   extern __shared__ __align__(16) char dyn0[];
   Scr* ss = (Scr*)dyn0;
@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(96, 1) k_serial(SerialArgs a, u32 nsets) {
     g_pf_cur = -1;
     g_pf_stop = 0;
     pipe.ready = 0;
+    pipe.books_done = 0;
     pipe.stop = 0;
     ss[0].win_done = ss[1].win_done = 0;
   }
@@ -762,7 +763,9 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
 #if defined(E2_SMEM_NODECACHE)
     const unsigned threads = 32;
 #else
-    const unsigned threads = (a.kind == 0 && !h->no_pipe) ? (h->no_prefetch ? 64 : 96) : 32;
+    const unsigned threads = (a.kind == 0 && !h->no_pipe) ? 128 : 32;  // warps: decide, evict, prefetch, books
+    SerialArgs& am = const_cast<SerialArgs&>(a);
+    am.no_prefetch = h->no_prefetch ? 1 : 0;
 #endif
     k_serial<<<1, threads, h->serial_smem, h->stream>>>(a, h->nsets);
     CK(cudaGetLastError());
