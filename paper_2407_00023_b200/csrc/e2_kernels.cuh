@@ -353,6 +353,9 @@ E2_D void api_op(Scr* s, const OpDesc& op0, const u32* hint, int nh, ApiOut* out
   }
 }
 
+#ifndef E2_DEFER_LRU
+#define E2_DEFER_LRU false  // true: the path's LRU re-indexing runs on warp 1 before its evictions (faster before the bookkeeping warp; now ~2% slower on C2)
+#endif
 #define PHASE_T0() PHASE_MARK(15)
 #define PHASE(i) PHASE_MARK(i)
 
@@ -757,7 +760,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       }
       wsync();
       pre_done = defer && i + 1 < a.n;
-      ok = dec.ok && replay_main(s, a, i, now, dec, &w, true, defer);
+      ok = dec.ok && replay_main(s, a, i, now, dec, &w, E2_DEFER_LRU, defer);
       // not deferred (round robin, very deep paths): the commit wrote the
       // inflight record itself; only then may warp 1 apply note_finished
       if (dec.ok && !defer) {
