@@ -132,6 +132,13 @@ inline double i2d(i64 v) { return (double)v; }
 
 E2_HD bool lane0() { return lane() == 0; }
 
+// Block-scope memory fence (hand-off flags between the replay's warps)
+#if E2_DEVICE_BUILD
+E2_D void fence_block() { __threadfence_block(); }
+#else
+inline void fence_block() {}
+#endif
+
 // L1 prefetch of a global address (no-op in the host emulation)
 #if E2_DEVICE_BUILD
 E2_D void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }

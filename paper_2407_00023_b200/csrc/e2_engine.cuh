@@ -1225,8 +1225,11 @@ E2_DNI u64 path_update(u32 tail, int g, double now, bool mark) {
 // tail slot.
 // defer_inflight: the inflight sums and record are left to the caller
 // (the pipelined replay's second warp, inflight_insert).
+// fix_flag: raised (to fix_val) as soon as the path's deferred LRU
+// re-indexing may start (s_path->fix_D), before the path log is written.
 E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 req_id, double arrival,
-                  double now, bool mark, Scr* s_path, bool defer_lru = false, bool defer_inflight = false) {
+                  double now, bool mark, Scr* s_path, bool defer_lru = false, bool defer_inflight = false,
+                  volatile long long* fix_flag = nullptr, long long fix_val = 0) {
   const bool win_done = s_path && s_path->win_done;
   if (s_path && lane0()) {
     s_path->fix_D = 0;
@@ -1274,6 +1277,13 @@ E2_DNI u32 commit(i64 seq_off, i64 n, i64 L, const Walk& w, const Dec& r, i64 re
     if (lane0()) s_path->cpath = D;
     // levels past kMaxPath live in the single global overflow: not deferrable
     root_id = path_update_par(s_path, D, g, now, mark, defer_lru && D <= kMaxPath);
+    if (fix_flag) {
+      if (lane0()) {
+        fence_block();
+        *fix_flag = fix_val;
+      }
+      wsync();
+    }
     PHASE_MARK(10);
     plen = plog_append(s_path, D, g);
   } else {

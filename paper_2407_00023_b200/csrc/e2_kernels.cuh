@@ -354,7 +354,7 @@ E2_D void api_op(Scr* s, const OpDesc& op0, const u32* hint, int nh, ApiOut* out
 }
 
 #ifndef E2_DEFER_LRU
-#define E2_DEFER_LRU false  // true: the path's LRU re-indexing runs on warp 1 before its evictions (faster before the bookkeeping warp; now ~2% slower on C2)
+#define E2_DEFER_LRU true  // the path's LRU re-indexing runs on warp 1 beside the rest of the commit
 #endif
 #define PHASE_T0() PHASE_MARK(15)
 #define PHASE(i) PHASE_MARK(i)
@@ -387,7 +387,7 @@ E2_D double replay_pre(Scr* s, const SerialArgs& a, i64 li) {
 // spec_w: a speculative decide of this request already validated by the
 // pipeline (its Walk and Scr path are current), or null.
 E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec, const Walk* spec_w = nullptr,
-                      bool defer_lru = false, bool defer_inflight = false) {
+                      bool defer_lru = false, bool defer_inflight = false, volatile long long* fix_flag = nullptr) {
   const i64 r = a.base + li;
   const i64 off = a.off[r], n = a.len[r];
   const i32* seq = DEV.tok + off;
@@ -401,7 +401,8 @@ E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec,
   if (!dec.ok) return false;
   PHASE(1);
   const bool fuse = a.prefill && DEV.cfg.mode == 0;  // note_prefill_cached(p, d.gpu, now) folded in
-  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s, defer_lru, defer_inflight);
+  const u32 tail = commit(off, n, a.L[li], w, dec, a.ids[r], a.arr[r], now, fuse, s, defer_lru, defer_inflight,
+                          fix_flag, li + 1);
   if (HOT.err) return false;
   PHASE(2);
   if (lane0()) DEV.req_tail[r] = tail;
@@ -498,6 +499,9 @@ struct Pipe {
   // are applied by warp 1 once warp 0 raises `ready` (= request index + 1)
   volatile long long ready;
   volatile long long books_done;  // warp 3: bookkeeping of requests [0, books_done) applied
+  volatile long long fix_ready;   // warp 0: request fix_ready-1's path is updated (LRU fixes may start)
+  const Scr* fs;                  // that request's scratch (deferred LRU fixes)
+  i32 fg;                         // and instance
   i64 c_id, c_cached, c_n;
   u64 c_root;
   double c_arr, c_now;
@@ -672,6 +676,11 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       PHASE_MARK1(23);  // waiting
       if (have) replay_out(psb, a, pli, pdec);
       PHASE_MARK1(22);  // decision record
+      // the LRU re-indexing of the path warp 0 is committing, beside the
+      // rest of its commit (it must precede this warp's evictions)
+      while (pp->fix_ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
+      if (pp->fix_ready == ci + 1 && pp->fs->fix_D > 0) path_lru_fix(pp->fs, pp->fs->fix_D, pp->fg);
+      PHASE_MARK1(20);  // LRU fixes
       bar_pair(2);
       PHASE_MARK1(23);
       if (pp->stop) break;
@@ -682,8 +691,6 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       pdec = pp->dec;
       psb = sb;
       have = true;
-      if (sb->fix_D > 0) path_lru_fix(sb, sb->fix_D, pp->g);
-      PHASE_MARK1(20);  // LRU fixes
       replay_evict(a, pp->li, pp->g);
       PHASE_MARK1(21);  // evictions
     }
@@ -760,7 +767,20 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       }
       wsync();
       pre_done = defer && i + 1 < a.n;
-      ok = dec.ok && replay_main(s, a, i, now, dec, &w, E2_DEFER_LRU, defer);
+      if (lane0()) {
+        pp->fs = s;
+        pp->fg = dec.gpu;
+        s->fix_D = 0;  // nothing to re-index unless path_update_par defers it
+      }
+      wsync();
+      ok = dec.ok && replay_main(s, a, i, now, dec, &w, E2_DEFER_LRU, defer, E2_DEFER_LRU ? &pp->fix_ready : nullptr);
+      // commits that raised no hand-off (no level-parallel path update, round
+      // robin, a failed decide): release warp 1 with nothing to re-index
+      if (lane0() && pp->fix_ready != i + 1) {
+        __threadfence_block();
+        pp->fix_ready = i + 1;
+      }
+      wsync();
       // not deferred (round robin, very deep paths): the commit wrote the
       // inflight record itself; only then may warp 1 apply note_finished
       if (dec.ok && !defer) {

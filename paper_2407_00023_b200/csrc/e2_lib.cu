@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
     g_pf_stop = 0;
     pipe.ready = 0;
     pipe.books_done = 0;
+    pipe.fix_ready = 0;
     pipe.stop = 0;
     ss[0].win_done = ss[1].win_done = 0;
   }
