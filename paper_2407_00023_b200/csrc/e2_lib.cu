@@ -765,10 +765,10 @@ void launch_serial(e2_handle* h, const SerialArgs& a) {
     const unsigned threads = 32;
 #else
     const unsigned threads = (a.kind == 0 && !h->no_pipe) ? 128 : 32;  // warps: decide, evict, prefetch, books
-    SerialArgs& am = const_cast<SerialArgs&>(a);
-    am.no_prefetch = h->no_prefetch ? 1 : 0;
+    SerialArgs ka = a;
+    ka.no_prefetch = h->no_prefetch ? 1 : 0;
 #endif
-    k_serial<<<1, threads, h->serial_smem, h->stream>>>(a, h->nsets);
+    k_serial<<<1, threads, h->serial_smem, h->stream>>>(ka, h->nsets);
     CK(cudaGetLastError());
 #else
     Scr s;
