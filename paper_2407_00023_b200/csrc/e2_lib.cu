@@ -122,7 +122,10 @@ void grow(T*& p, size_t keep, size_t n, Stream s) {
 namespace {
 
 constexpr int kMatchWarpsPerBlock = 8;
-constexpr i64 kFirstBatch = 2048;  // replay batch-size ramp start
+#ifndef E2_FIRST_BATCH
+#define E2_FIRST_BATCH 2048
+#endif
+constexpr i64 kFirstBatch = E2_FIRST_BATCH;  // replay batch-size ramp start
 constexpr size_t kScrBytes = (2 * sizeof(Scr) + 127) / 128 * 128;
 
 #if E2_DEVICE_BUILD
