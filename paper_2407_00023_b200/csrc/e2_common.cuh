@@ -66,6 +66,8 @@ template <typename T>
 E2_D T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 template <typename T>
 E2_D T shfl_up1(T v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+template <typename T>
+E2_D T shfl_down1(T v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 E2_D int ffs32(u32 m) { return __ffs((int)m) - 1; }
 E2_D int popc32(u32 m) { return __popc(m); }
 E2_D int popc64(u64 m) { return __popcll(m); }
@@ -88,6 +90,8 @@ template <typename T>
 E2_D T shfl(T v, int) { return v; }
 template <typename T>
 E2_D T shfl_up1(T v) { return v; }
+template <typename T>
+E2_D T shfl_down1(T v) { return v; }
 E2_D int ffs32(u32 m) { return __ffs((int)m) - 1; }
 E2_D int popc32(u32 m) { return __popc(m); }
 E2_D int popc64(u64 m) { return __popcll(m); }
@@ -107,6 +111,8 @@ template <typename T>
 inline T shfl(T v, int) { return v; }
 template <typename T>
 inline T shfl_up1(T v) { return v; }
+template <typename T>
+inline T shfl_down1(T v) { return v; }
 inline int ffs32(u32 m) { return m ? __builtin_ctz(m) : -1; }
 inline int popc32(u32 m) { return __builtin_popcount(m); }
 inline int popc64(u64 m) { return __builtin_popcountll(m); }

@@ -752,19 +752,35 @@ E2_DNI void path_lru_fix(const Scr* s, int D, int g) {
 // defer: leave the LRU re-indexing to path_lru_fix (s->fix_D = D).
 E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark, bool defer = false) {
   const int G = DEV.cfg.G;
-  // pass 1: which nodes become cached (a parent's count uses its child's flag)
-  for (int i = lane(); i < D; i += kWidth) {
-    const NodeRec* r = npeek(PSLOT(s, i));
-    PFLAG(s, i) = (mark && !rcached(r, g)) ? 1u : 0u;
+  // the parent's cached-child count uses its child's "newly cached" flag:
+  // one lane per level, the child's flag from the next lane (one pass) when
+  // the path fits a warp, else from a first pass through shared memory
+  const bool onepass = E2_WARP && D <= kWidth;
+  if (!onepass) {
+    for (int i = lane(); i < D; i += kWidth) {
+      const NodeRec* r = npeek(PSLOT(s, i));
+      PFLAG(s, i) = (mark && !rcached(r, g)) ? 1u : 0u;
+    }
+    wsync();
   }
-  wsync();
   i64 add = 0;
   u32 any = 0;
-  for (int i = lane(); i < D; i += kWidth) {
-    NodeRec* r = npoke(PSLOT(s, i));
-    const bool newly = PFLAG(s, i) & 1u;
-    const bool inc = i + 1 < D && (PFLAG(s, i + 1) & 1u);
-    const bool was = rcached(r, g);
+  u64 id0 = 0;
+  for (int b = 0; b < D; b += kWidth) {
+    const int i = b + lane();
+    const bool in = i < D;
+    NodeRec* r = in ? npoke(PSLOT(s, i)) : nullptr;
+    const bool was = in && rcached(r, g);
+    bool newly, inc;
+    if (onepass) {
+      newly = in && mark && !was;
+      inc = (shfl_down1((int)newly) != 0) && i + 1 < D;
+    } else {
+      newly = in && (PFLAG(s, i) & 1u);
+      inc = in && i + 1 < D && (PFLAG(s, i + 1) & 1u);
+    }
+    if (i == 0) id0 = r->id;
+    if (!in) continue;
     const i32 ccc0 = rccc(r, G)[g];
     const i32 ccc1 = ccc0 + (inc ? 1 : 0);
     const double la0 = rla(r)[g];
@@ -788,6 +804,7 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark, bool def
 #if E2_WARP
   add = warp_sum(add);
   any = ballot(any != 0) ? 1u : 0u;
+  id0 = shfl(id0, 0);
 #endif
   wsync();
   if (lane0()) HOT.cached_tokens[g] += add;
@@ -803,7 +820,7 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark, bool def
   } else if (any) {
     path_lru_fix(s, D, g);
   }
-  return D > 0 ? nget(PSLOT(s, 0))->id : 0;
+  return D > 0 ? id0 : 0;
 }
 
 // ensure_path (prefix_tree.cpp:156-185) given the walk of the same sequence.
