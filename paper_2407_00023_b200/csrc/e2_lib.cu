@@ -126,6 +126,13 @@ constexpr int kMatchWarpsPerBlock = 8;
 #define E2_FIRST_BATCH 2048
 #endif
 constexpr i64 kFirstBatch = E2_FIRST_BATCH;  // replay batch-size ramp start
+#ifndef E2_SHORT_FIRST_BATCH
+#define E2_SHORT_FIRST_BATCH 256
+#endif
+// short replays (at most 4 first batches) start the ramp lower: there the
+// cold-tree first batch is most of the trace, and K1 launch latency is cheap
+// next to hint-less walks
+constexpr i64 kShortFirstBatch = E2_SHORT_FIRST_BATCH;
 constexpr size_t kScrBytes = (2 * sizeof(Scr) + 127) / 128 * 128;
 
 #if E2_DEVICE_BUILD
@@ -1862,7 +1869,7 @@ int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, con
     // Batch sizes ramp up geometrically from kFirstBatch: a batch is matched
     // against the tree at its start, so early batches (a cold tree) would
     // leave most requests without K1 path hints.
-    i64 cur_b = std::min<i64>(B, kFirstBatch);
+    i64 cur_b = std::min<i64>(B, n <= 4 * kFirstBatch ? kShortFirstBatch : kFirstBatch);
     for (i64 b0 = 0; b0 < n; b0 += cur_b, cur_b = std::min<i64>(B, cur_b * 2)) {
       const i64 nb = std::min<i64>(cur_b, n - b0);
       launch_match(h, b0, nb);
