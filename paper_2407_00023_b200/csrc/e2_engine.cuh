@@ -1021,7 +1021,7 @@ E2_D Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint
   }
   if (!spec && lane0()) HOT.stats[kStTreeReads]++;  // a validated speculative decide is counted by the caller
   wsync();
-  PHASE_MARK(1);
+  PHASE_MARK(32);
   w = walk_par(seq, L, hint, nhint, s, hS, lead, hint_rows);
   if (!w.ok && s->npath < 0) {
     if (spec) SPEC_FAIL();
@@ -1065,7 +1065,7 @@ E2_D Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint
       if (s->ext[g] == best) cand |= (1ull << g);
     }
 #endif
-    PHASE_MARK(1);
+    PHASE_MARK(33);
     if (spec && any_need(s, cand, n)) SPEC_FAIL();
     cost_prepare_set(s, cand, n, now);
     PHASE_MARK(7);

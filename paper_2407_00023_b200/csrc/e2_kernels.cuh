@@ -415,6 +415,7 @@ E2_D bool replay_main(Scr* s, const SerialArgs& a, i64 li, double now, Dec& dec,
     for (int l = lane(); l <= nw; l += kWidth) row[l] = l < nw ? PSLOT(s, l) : kNil;
   }
   wsync();
+  PHASE(36);  // hint row
   return true;
 }
 
@@ -679,6 +680,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       // the LRU re-indexing of the path warp 0 is committing, beside the
       // rest of its commit (it must precede this warp's evictions)
       while (pp->fix_ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
+      PHASE_MARK1(31);  // waiting for warp 0's path update
       if (pp->fix_ready == ci + 1 && pp->fs->fix_D > 0) path_lru_fix(pp->fs, pp->fs->fix_D, pp->fg);
       PHASE_MARK1(20);  // LRU fixes
       bar_pair(2);
@@ -704,8 +706,10 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     if (lane0()) g_pf_cur = i;
     // warp 3 applied request i-1's bookkeeping (and, if deferred, prepared
     // this request's `now` and loads)
-    if (i > 0)
+    if (i > 0) {
       while (pp->books_done < i) __nanosleep(32);
+      PHASE(30);  // waiting for warp 3's bookkeeping
+    }
     const double now = pre_done ? s->pre_now : replay_pre(s, a, i);
     // decide speculatively while warp 1 evicts for request i-1
     Dec dec;
@@ -729,6 +733,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     if (valid) {
       if (DEV.cfg.mode == 0 && lane0()) HOT.stats[kStTreeReads]++;
       wsync();
+      PHASE(34);  // validation
     } else {
       PHASE_COUNT(17);  // speculation redone
       const i64 r = a.base + i;
@@ -767,6 +772,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       }
       wsync();
       pre_done = defer && i + 1 < a.n;
+      PHASE(35);  // hand-off
       if (lane0()) {
         pp->fs = s;
         pp->fg = dec.gpu;
@@ -803,7 +809,9 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       pp->s = s;
     }
     wsync();
+    PHASE(37);
     bar_pair(2);
+    PHASE(18);  // waiting for warp 1's LRU fixes / decision record
     past1 = false;
   }
   if (!past1) bar_pair(1);  // wait for the last evict

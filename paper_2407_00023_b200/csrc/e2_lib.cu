@@ -1955,7 +1955,7 @@ int e2_profile_reset(e2_handle* h, int32_t enable_timing) {
 extern "C" int e2_debug_phases(e2_handle* h, uint64_t* out) {
   return guard(h, [&] {
     pull_hot(h);
-    for (int i = 0; i < 32; ++i) out[i] = h->hot.phase_cycles[i];
+    for (int i = 0; i < 40; ++i) out[i] = h->hot.phase_cycles[i];
   });
 }
 #endif

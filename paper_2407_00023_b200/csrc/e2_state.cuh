@@ -176,7 +176,7 @@ struct Hot {
   i32 err, why;
   i64 err_req;  // request index / op index that failed
   i64 done;     // ops fully processed in the last launch
-  u64 phase_cycles[32];  // E2_PHASES builds: clock64 per replay phase
+  u64 phase_cycles[40];  // E2_PHASES builds: clock64 per replay phase
   u64 phase_last, phase_last1;
 };
 static_assert(sizeof(Hot) % 8 == 0, "Hot is copied as u64 words");
