@@ -815,7 +815,7 @@ void note_depth(e2_handle* h, u64 levels) {
 void launch_match(e2_handle* h, i64 base, i64 n) {
   if (n == 0) return;
   reserve_batch(h, n);
-  Dev& d = h->d;
+  [[maybe_unused]] Dev& d = h->d;  // the host emulation's match reads the arena through it
 #if E2_DEVICE_BUILD
   {
     const i64 blocks = (n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock;
@@ -1401,7 +1401,6 @@ const char* e2_last_error(const e2_handle* h) { return h ? h->err.c_str() : g_er
 int e2_reset(e2_handle* h) {
   return guard(h, [&] {
     Dev& d = h->d;
-    const int G = h->G;
     const u64 used = h->hot.slots_used;
     dset(d.rec, 0, used * d.rs, h->stream);
     {
