@@ -509,6 +509,13 @@ struct Pipe {
   i32 c_g, c_defer;
 };
 
+#ifndef E2_WAIT_NS
+#define E2_WAIT_NS 32  // back-off of the hand-off polls (0: spin)
+#endif
+E2_D void wait_pause() {
+  if (E2_WAIT_NS > 0) __nanosleep(E2_WAIT_NS);
+}
+
 E2_D void bar_pair(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 // Warp 0, after barrier 1: did the eviction that ran beside a speculative
@@ -634,7 +641,7 @@ E2_D void prefetch_loop(const SerialArgs& a) {
 // tree, warp 1 writes the decision record or evicts).
 E2_D void books_loop(Scr* s2, const SerialArgs& a, Pipe* pp) {
   for (i64 ci = 0;; ++ci) {
-    while (pp->ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
+    while (pp->ready != ci + 1 && !*(volatile i32*)&pp->stop) wait_pause();
     if (pp->ready != ci + 1) break;
     if (pp->c_defer) inflight_insert(pp->c_id, pp->c_g, pp->c_cached, pp->c_n, pp->c_arr, pp->c_root);
     replay_finish(a, ci, pp->c_now);
@@ -679,7 +686,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       PHASE_MARK1(22);  // decision record
       // the LRU re-indexing of the path warp 0 is committing, beside the
       // rest of its commit (it must precede this warp's evictions)
-      while (pp->fix_ready != ci + 1 && !*(volatile i32*)&pp->stop) __nanosleep(32);
+      while (pp->fix_ready != ci + 1 && !*(volatile i32*)&pp->stop) wait_pause();
       PHASE_MARK1(31);  // waiting for warp 0's path update
       if (pp->fix_ready == ci + 1 && pp->fs->fix_D > 0) path_lru_fix(pp->fs, pp->fs->fix_D, pp->fg);
       PHASE_MARK1(20);  // LRU fixes
@@ -707,7 +714,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     // warp 3 applied request i-1's bookkeeping (and, if deferred, prepared
     // this request's `now` and loads)
     if (i > 0) {
-      while (pp->books_done < i) __nanosleep(32);
+      while (pp->books_done < i) wait_pause();
       PHASE(30);  // waiting for warp 3's bookkeeping
     }
     const double now = pre_done ? s->pre_now : replay_pre(s, a, i);
