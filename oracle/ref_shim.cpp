@@ -13,6 +13,7 @@
 //   mirror :121, redirects :122, stats :123; load_cost (cost_model.hpp:87-89);
 //   generate / assign_poisson_arrivals (workload.hpp:80,109).
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -37,6 +38,18 @@ struct e2_handle {
 namespace {
 
 thread_local std::string g_create_err;
+
+}  // namespace
+
+// csrc/workload_gen.cpp compiled with -DE2_GEN_PREFIXED (oracle/Makefile)
+extern "C" void e2gen_e2_workload_default_impl(int32_t archetype, e2_workload_spec* out);
+extern "C" int e2gen_e2_generate_impl(const e2_workload_spec* spec, uint64_t seed, double rps,
+                              uint64_t arrival_seed, int64_t* n_requests, int64_t* n_tokens,
+                              int32_t* tokens, int64_t* offsets, int64_t* ids, double* arrivals,
+                              int64_t* output_lens);
+void e2_set_global_error(const char* m) { g_create_err = m; }
+
+namespace {
 
 SchedulerConfig to_cfg(const e2_sched_cfg* c) {
   SchedulerConfig s;
@@ -444,6 +457,66 @@ int e2_replay(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const
   return rc;
 }
 
+// Timing entry for bench.py's reference arm (not part of e2sched.h): the
+// criterion-7 loop exactly as acceptance_main.cpp:367-416 times it.  The
+// Request objects are built before the clock starts (to_requests at :378 is
+// outside the reference's timed region too), no extra mirror().match() is
+// taken and decisions are not copied out; *seconds = steady_clock time of
+// the scheduling loop alone.  Mirror-LRU eviction (E4) replaces the FIFO
+// block when drv->eviction asks for it.
+int e2ref_time_loop(e2_handle* h, const int32_t* tokens, const int64_t* offsets,
+                    const int64_t* ids, const double* arrivals, const int64_t* output_lens,
+                    int64_t n, const e2_driver_cfg* drv, double* seconds, int64_t* n_done) {
+  if (n_done) *n_done = 0;
+  GlobalScheduler& s = *h->s;
+  std::vector<Request> reqs(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    reqs[i].id = ids[i];
+    reqs[i].arrival_ms = arrivals[i];
+    reqs[i].prompt.assign(tokens + offsets[i], tokens + offsets[i + 1]);
+    reqs[i].output_len = output_lens[i];
+  }
+  std::vector<std::deque<std::pair<const TokenSeq*, int64_t>>> cached(h->n);
+  int64_t i = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  int rc = guard(h, [&] {
+    SimTime now = 0;
+    t0 = std::chrono::steady_clock::now();
+    for (i = 0; i < n; ++i) {
+      const Request& r = reqs[i];
+      now = std::max(now, r.arrival_ms);
+      const Decision d = s.schedule_request(r, now);
+      if (drv->prefill_cached) s.note_prefill_cached(r.prompt, d.gpu, now);
+      if (drv->eviction == E2_EVICT_FIFO_TAIL) {
+        cached[d.gpu].push_back({&r.prompt, static_cast<int64_t>(r.prompt.size()) - drv->trunk_len});
+        while (s.mirror().cached_tokens(d.gpu) > drv->high_water && !cached[d.gpu].empty()) {
+          EvictedRange range;
+          range.seq = *cached[d.gpu].front().first;
+          range.tail_len = cached[d.gpu].front().second;
+          cached[d.gpu].pop_front();
+          s.note_eviction(range, d.gpu, now);
+        }
+      } else if (drv->eviction == E2_EVICT_MIRROR_LRU) {
+        const int64_t c = s.mirror().cached_tokens(d.gpu);
+        if (c > drv->high_water) {
+          EvictionPlan plan = s.mirror().plan_eviction(d.gpu, c - drv->high_water, {}, true);
+          std::vector<EvictedRange> ranges;
+          for (const auto& e : plan.entries) ranges.push_back({s.mirror().path_tokens(e.node), e.tokens});
+          for (const auto& rg : ranges) s.note_eviction(rg, d.gpu, now);
+        }
+      }
+      if (i >= drv->finish_lag) {
+        const Request& old = reqs[i - drv->finish_lag];
+        s.note_finished(old.id, now, old.output_len);
+      }
+    }
+  });
+  if (seconds)
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (n_done) *n_done = i;
+  return rc;
+}
+
 int e2_replay_device(e2_handle* h, const int32_t*, const int64_t*, const int64_t*, const double*,
                      const int64_t*, int64_t, const e2_driver_cfg*, e2_decision*, e2_cost*, double*,
                      void*, int64_t*) {
@@ -460,6 +533,10 @@ int e2_profile_get(e2_handle* h, e2_profile* out) {
 int e2_profile_reset(e2_handle*, int32_t) { return E2_OK; }
 
 void e2_workload_default(int32_t archetype, e2_workload_spec* out) {
+  if (archetype == E2_ARCH_TREE_OF_THOUGHT) {
+    e2gen_e2_workload_default_impl(archetype, out);
+    return;
+  }
   std::memset(out, 0, sizeof(*out));
   Archetype a = Archetype::Custom;
   switch (archetype) {
@@ -499,11 +576,14 @@ int e2_generate(const e2_workload_spec* spec, uint64_t seed, double rps, uint64_
     case E2_ARCH_PROGRAMMING: a = Archetype::Programming; break;
     case E2_ARCH_VIDEO_QA: a = Archetype::VideoQa; break;
     case E2_ARCH_DOC_QA: a = Archetype::DocQa; break;
-    default: g_create_err = "archetype not in the reference"; return E2_ERR_ARG;
+    default: a = Archetype::Custom; break;
   }
-  if (spec->branch_len_max > spec->branch_len) {
-    g_create_err = "variable trunk lengths are not a reference feature";
-    return E2_ERR_ARG;
+  if (spec->archetype == E2_ARCH_TREE_OF_THOUGHT || spec->branch_len_max > spec->branch_len) {
+    // Shapes the reference generator lacks: the
+    // repo's generator, linked into this library (oracle/Makefile), so a
+    // reference-only process needs no product library for its input.
+    return e2gen_e2_generate_impl(spec, seed, rps, arrival_seed, n_requests, n_tokens, tokens, offsets, ids,
+                          arrivals, output_lens);
   }
   try {
     WorkloadSpec s;

@@ -10,13 +10,21 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
-#include <map>
 #include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "e2sched.h"
+
+// The test-only reference shim (oracle/ref_shim.cpp) links this generator
+// under other names for the archetypes the reference lacks, so the bench's
+// reference arm never maps the product library (oracle/Makefile).
+#ifdef E2_GEN_PREFIXED
+#define E2_GEN_NAME(x) e2gen_##x##_impl
+#else
+#define E2_GEN_NAME(x) x
+#endif
 
 namespace {
 
@@ -164,31 +172,47 @@ void build(const e2_workload_spec& s, uint64_t seed, Builder& b) {
       break;
     }
     case E2_ARCH_TREE_OF_THOUGHT: {
-      // Problems arrive in blocks of requests_per_group; each request follows
-      // a random root-to-node path of a fanout^depth thought tree whose
-      // segments get fresh token ids on first visit.
+      // Problems arrive in blocks of requests_per_group.  Each problem owns a
+      // thought tree of the given fanout and depth; a request follows a random
+      // root-to-node path of k ~ U[1, depth] thoughts (a thought's tokens are
+      // fresh ids, U[unique_min, unique_max] of them, drawn on its first
+      // visit) and ends with observation_len fresh tokens of its own (the
+      // step instruction), so every request adds a leaf to the radix tree and
+      // every visited thought where paths end or fork becomes a node
+      // boundary.  Thought tree per problem: flat arrays, children by index.
       const int64_t per = std::max<int64_t>(1, std::llround(s.requests_per_group));
       const int64_t fan = std::max<int64_t>(1, s.fanout), dep = std::max<int64_t>(1, s.depth);
       int64_t made = 0, group = 0;
+      std::vector<int64_t> child, seg_base, seg_len;
       while (made < N) {
         const int64_t size = std::min(per, N - made);
         const std::vector<int32_t> trunk = id_run(kTrunk + group * s.branch_len, s.branch_len);
-        std::map<std::vector<int64_t>, std::vector<int32_t>> seg;
+        child.assign((size_t)fan, -1);  // node 0: the problem root
+        seg_base.assign(1, 0);
+        seg_len.assign(1, 0);
         for (int64_t j = 0; j < size; ++j) {
           std::vector<int32_t> p = sys;
           p.insert(p.end(), trunk.begin(), trunk.end());
           const int64_t k = span(1, dep, rng);
-          std::vector<int64_t> path;
+          int64_t cur = 0;
           for (int64_t l = 0; l < k; ++l) {
-            path.push_back(span(0, fan - 1, rng));
-            auto it = seg.find(path);
-            if (it == seg.end()) {
-              std::vector<int32_t> v;
-              b.fresh_ids(v, span(s.unique_min, s.unique_max, rng));
-              it = seg.emplace(path, std::move(v)).first;
+            const int64_t c = span(0, fan - 1, rng);
+            int64_t nx = child[(size_t)(cur * fan + c)];
+            if (nx < 0) {
+              nx = (int64_t)seg_base.size();
+              child[(size_t)(cur * fan + c)] = nx;
+              child.resize(child.size() + (size_t)fan, -1);
+              const int64_t n = span(s.unique_min, s.unique_max, rng);
+              seg_base.push_back(b.fresh);
+              seg_len.push_back(n);
+              std::vector<int32_t> tmp;
+              b.fresh_ids(tmp, n);
             }
-            p.insert(p.end(), it->second.begin(), it->second.end());
+            const int64_t sb = seg_base[(size_t)nx], sl = seg_len[(size_t)nx];
+            for (int64_t t = 0; t < sl; ++t) p.push_back((int32_t)(sb + t));
+            cur = nx;
           }
+          b.fresh_ids(p, s.observation_len);
           b.emit(p, span(s.output_min, s.output_max, rng));
         }
         made += size;
@@ -205,7 +229,7 @@ void e2_set_global_error(const char* m);
 
 extern "C" {
 
-void e2_workload_default(int32_t archetype, e2_workload_spec* o) {
+void E2_GEN_NAME(e2_workload_default)(int32_t archetype, e2_workload_spec* o) {
   memset(o, 0, sizeof(*o));
   o->archetype = archetype;
   o->request_count = 1000;
@@ -257,13 +281,14 @@ void e2_workload_default(int32_t archetype, e2_workload_spec* o) {
       o->output_max = 30;
       break;
     case E2_ARCH_TREE_OF_THOUGHT:
-      o->system_prompt_len = 1000;
-      o->branch_len = 500;
-      o->requests_per_group = 64.0;
+      o->system_prompt_len = 500;
+      o->branch_len = 300;
+      o->requests_per_group = 128.0;
       o->fanout = 3;
-      o->depth = 8;
-      o->unique_min = 40;
-      o->unique_max = 120;
+      o->depth = 16;
+      o->unique_min = 30;
+      o->unique_max = 90;
+      o->observation_len = 24;
       o->output_min = 40;
       o->output_max = 120;
       break;
@@ -273,7 +298,7 @@ void e2_workload_default(int32_t archetype, e2_workload_spec* o) {
   o->branch_len_max = o->branch_len;
 }
 
-int e2_generate(const e2_workload_spec* spec, uint64_t seed, double rps, uint64_t arrival_seed, int64_t* n_requests,
+int E2_GEN_NAME(e2_generate)(const e2_workload_spec* spec, uint64_t seed, double rps, uint64_t arrival_seed, int64_t* n_requests,
                 int64_t* n_tokens, int32_t* tokens, int64_t* offsets, int64_t* ids, double* arrivals,
                 int64_t* output_lens) {
   try {
