@@ -252,6 +252,40 @@ int e2_replay_device(e2_handle* h, const int32_t* d_tokens, const int64_t* d_off
                      e2_decision* d_out, e2_cost* d_costs, double* d_ratios, void* stream,
                      int64_t* n_done);
 
+/* ---------------------------------------------------------------------------
+ * Sharded replay (product only).  The reference scheduler is
+ * single-threaded and has no counterpart: this is the multi-GPU form of the
+ * batched replay above (acceptance_main.cpp:367-416 generalised).  Every rank
+ * holds a replica of the tree and the whole trace in its own HBM.  Per batch:
+ *   all ranks: e2_shard_next (the batch bounds; identical on every rank),
+ *              e2_shard_match on the rank's contiguous slice [lo, lo+cnt)
+ *              (K1), writing a summary slice of 16 + per*row_bytes bytes;
+ *   caller:    gathers the world's slices, rank-major, to rank 0 (NCCL);
+ *   rank 0:    e2_shard_commit (leader rounds + the serial decide/commit
+ *              pass + the state delta vs what the replicas hold), then
+ *              e2_shard_delta_copy into a device buffer of delta_bytes;
+ *   caller:    broadcasts the delta from rank 0 (NCCL);
+ *   replicas:  e2_shard_apply.  After it every replica's tree, LRU, windows
+ *              and counters equal rank 0's byte for byte.
+ * The loop ends when e2_shard_next returns nb == 0 (also after a failed
+ * batch: e2_shard_end then returns the batch's error on every rank).
+ * Decisions/costs are written on rank 0 only (device pointers).
+ * ------------------------------------------------------------------------- */
+int e2_shard_begin(e2_handle* h, const int32_t* d_tokens, const int64_t* d_offsets, const int64_t* d_ids,
+                   const double* d_arrivals, const int64_t* d_output_lens, int64_t n, const e2_driver_cfg* drv,
+                   e2_decision* d_out, e2_cost* d_costs, double* d_ratios, int32_t rank, int32_t world);
+int e2_shard_next(e2_handle* h, int64_t* b0, int64_t* nb, int64_t* row_bytes);
+int e2_shard_match(e2_handle* h, int64_t lo, int64_t cnt, void* d_slice);
+int e2_shard_commit(e2_handle* h, const void* d_gathered, int64_t per, int64_t* delta_bytes);
+int e2_shard_delta_copy(e2_handle* h, void* d_dst);
+int e2_shard_apply(e2_handle* h, const void* d_delta, int64_t bytes);
+int e2_shard_end(e2_handle* h, int64_t* n_done);
+/* Order-independent digest of every replicated state region plus the hot
+ * counters (n_out = regions + 1 values): equal digests on every rank after
+ * each e2_shard_apply is the replication invariant the tests check.  Does not
+ * mutate the state (unlike an export, which brings hit windows current). */
+int e2_state_digest(e2_handle* h, uint64_t* out, int32_t cap, int32_t* n_out);
+
 /* Product only: per-kernel device time (ms) and launch counts accumulated
  * since the last reset, for the bench's roofline (kernel ids below). */
 #define E2_K_MATCH 0  /* K1 batched prefix match */
@@ -264,6 +298,9 @@ typedef struct {
   int64_t launches[E2_K_COUNT];
   int64_t match_bytes;    /* algorithmic bytes of K1 */
   int64_t match_requests; /* requests K1 walked */
+  int64_t group_retries;  /* leader-round restarts after a grouping-hash collision */
+  int64_t delta_bytes;    /* sharded replay (rank 0): state-delta bytes exported */
+  int64_t delta_chunks;   /* sharded replay (rank 0): 64-byte chunks in those deltas */
 } e2_profile;
 int e2_profile_get(e2_handle* h, e2_profile* out);
 int e2_profile_reset(e2_handle* h, int32_t enable_timing);

@@ -136,6 +136,9 @@ class ProfileC(ctypes.Structure):
         ("launches", ctypes.c_int64 * E2_K_COUNT),
         ("match_bytes", ctypes.c_int64),
         ("match_requests", ctypes.c_int64),
+        ("group_retries", ctypes.c_int64),
+        ("delta_bytes", ctypes.c_int64),
+        ("delta_chunks", ctypes.c_int64),
     ]
 
 
@@ -206,8 +209,24 @@ _SIGS = {
     ),
 }
 
+#: Product-only entry points (the sharded replay); attached when
+#: the library exports them.
+_PRODUCT_SIGS = {
+    "e2_shard_begin": (
+        ctypes.c_int,
+        [_h, _vp, _vp, _vp, _vp, _vp, _i64, P(DriverCfg), _vp, _vp, _vp, _i32, _i32],
+    ),
+    "e2_shard_next": (ctypes.c_int, [_h, P(_i64), P(_i64), P(_i64)]),
+    "e2_shard_match": (ctypes.c_int, [_h, _i64, _i64, _vp]),
+    "e2_shard_commit": (ctypes.c_int, [_h, _vp, _i64, P(_i64)]),
+    "e2_shard_delta_copy": (ctypes.c_int, [_h, _vp]),
+    "e2_shard_apply": (ctypes.c_int, [_h, _vp, _i64]),
+    "e2_shard_end": (ctypes.c_int, [_h, P(_i64)]),
+    "e2_state_digest": (ctypes.c_int, [_h, _vp, _i32, P(_i32)]),
+}
+
 #: Every symbol include/e2sched.h declares (checked by the CPU test suite).
-DECLARED_SYMBOLS = tuple(_SIGS)
+DECLARED_SYMBOLS = tuple(_SIGS) + tuple(_PRODUCT_SIGS)
 
 _cache: dict[str, ctypes.CDLL] = {}
 
@@ -224,6 +243,11 @@ def load_library(path: str) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    for name, (res, args) in _PRODUCT_SIGS.items():
+        if hasattr(lib, name):
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
     _cache[path] = lib
     return lib
 

@@ -188,6 +188,10 @@ E2_D void subtree_apply(u32 root, int g, double now, bool mark) {
         return r->edge_len > 0 && r->parent == p;
       });
       wsync();
+      if (top + (u32)popc32(m) > DEV.vcap) {  // the host sizes vic_slot from its tree copy first
+        if (lane0()) set_err(kErrCapacity, kWhyScratchCap);
+        return;
+      }
       if (lane0()) {
         u32 mm = m, t = top;
         while (mm) {

@@ -26,6 +26,12 @@
 
 using namespace e2;
 
+#if !E2_DEVICE_BUILD
+struct uint4 {
+  unsigned int x, y, z, w;
+};
+#endif
+
 // ---------------------------------------------------------------------------
 // memory / launch layer
 // ---------------------------------------------------------------------------
@@ -240,7 +246,7 @@ __device__ __forceinline__ u32 gtab_find(const u64* tk, const u32* tv, u64 mask,
 
 __global__ void k_group_init(i64 n, i64 base, const i64* off, const i64* len, const i64* S, const u32* dslot,
                              const u32* dm, i32* state, u64* A, u64* B, i64* cand, i64* L, u64* tk, u32* tv,
-                             u64 mask, i64* leader) {
+                             u64 mask, i64* leader, int salt) {
   i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const i64 r = base + i;
@@ -255,7 +261,7 @@ __global__ void k_group_init(i64 n, i64 base, const i64* off, const i64* len, co
   A[i] = ((u64)dslot[i] << 32) | (u64)dm[i];
   B[i] = (u64)(u32)g_dev.tok[off[r] + s];
   cand[i] = s;
-  gtab_insert(tk, tv, mask, gkey(A[i], B[i], 0), (u32)i);
+  gtab_insert(tk, tv, mask, gkey(A[i], B[i], salt), (u32)i);
 }
 
 __global__ void k_group_resolve(i64 n, int round, i32* state, const u64* A, const u64* B, const i64* cand,
@@ -263,7 +269,7 @@ __global__ void k_group_resolve(i64 n, int round, i32* state, const u64* A, cons
                                 unsigned int* active, unsigned int* collide) {
   i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || state[i] != 1) return;
-  u32 m = gtab_find(tk, tv, mask, gkey(A[i], B[i], round));
+  u32 m = gtab_find(tk, tv, mask, gkey(A[i], B[i], round));  // round includes the attempt's salt
   if (m == kNil || A[m] != A[i] || B[m] != B[i]) {
     atomicAdd(collide, 1u);
     state[i] = 0;
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32)
       A[i] = ((u64)l << 32) | (u64)a;
       B[i] = (u64)(u32)g_dev.tok[off[r] + a];
       cand[i] = a;
-      gtab_insert(tk, tv, mask, gkey(A[i], B[i], round), (u32)i);
+      gtab_insert(tk, tv, mask, gkey(A[i], B[i], round), (u32)i);  // round includes the attempt's salt
     }
   }
 }
@@ -320,6 +326,155 @@ __global__ void k_arena_index(i64 n, i64 base_tok, const i64* offsets, i64* off,
 }
 #endif
 
+// ---- sharded replay: state delta + match summaries ----------
+// The replicated state is a fixed list of regions (node pool, child table,
+// LRU pages, windows, ...).  Rank 0 keeps a shadow copy of every region as
+// the replicas last received it; after each committed batch a diff pass
+// emits the 64-byte chunks that differ ({region<<48 | chunk} + payload), the
+// replicas scatter them (k_delta_apply) and rank 0 applies the same list to
+// its shadow.  Every allocation is zero-filled and every relayout (growth,
+// rehash) is a deterministic function of the state, so after the apply each
+// replica's regions equal rank 0's byte for byte.
+constexpr int kMaxRegions = 16;
+constexpr u32 kChunkWords = 16;  // 64 bytes
+struct RegionTab {
+  u32* cur[kMaxRegions];
+  const u32* sh[kMaxRegions];
+  u64 words[kMaxRegions];       // allocated words (apply bound)
+  u64 chunk0[kMaxRegions + 1];  // prefix sum of live chunks (diff)
+  u64 live_words[kMaxRegions];
+  int n;
+};
+
+E2_HDX int region_of(const RegionTab& t, u64 c) {
+  int r = 0;
+  while (r + 1 < t.n && c >= t.chunk0[r + 1]) ++r;
+  return r;
+}
+
+#if E2_DEVICE_BUILD
+// One thread per 16-byte quad, four quads per chunk (lanes 4k..4k+3).
+__global__ void __launch_bounds__(256) k_delta_diff(RegionTab t, u64 quads, u64* idx, uint4* pay, u64 cap,
+                                                    unsigned long long* count) {
+  for (u64 q0 = (u64)blockIdx.x * blockDim.x; q0 < quads; q0 += (u64)gridDim.x * blockDim.x) {
+    const u64 q = q0 + threadIdx.x;
+    const bool in = q < quads;
+    const u64 c = q >> 2;
+    const u32 part = (u32)(q & 3);
+    bool diff = false;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    int r = 0;
+    u64 cc = 0;
+    if (in) {
+      r = region_of(t, c);
+      cc = c - t.chunk0[r];
+      const u64 w = cc * kChunkWords + part * 4;
+      const u64 lw = t.live_words[r];
+      if (w + 4 <= lw) {
+        v = *(const uint4*)(t.cur[r] + w);
+        const uint4 o = *(const uint4*)(t.sh[r] + w);
+        diff = v.x != o.x || v.y != o.y || v.z != o.z || v.w != o.w;
+      } else if (w < lw) {
+        u32 vv[4] = {0, 0, 0, 0};
+        for (u64 k = 0; k < 4 && w + k < lw; ++k) {
+          vv[k] = t.cur[r][w + k];
+          diff |= vv[k] != t.sh[r][w + k];
+        }
+        v = make_uint4(vv[0], vv[1], vv[2], vv[3]);
+      }
+    }
+    // any quad of the chunk differs -> the whole chunk goes
+    const unsigned lane_id = threadIdx.x & 31;
+    const unsigned grp = 0xfu << (lane_id & ~3u);
+    const unsigned any = __ballot_sync(0xffffffffu, diff) & grp;
+    const bool lead = in && part == 0 && any != 0;
+    const unsigned leads = __ballot_sync(0xffffffffu, lead);
+    unsigned long long base = 0;
+    if (lane_id == 0 && leads) base = atomicAdd(count, (unsigned long long)__popc(leads));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const u64 slot = base + (u64)__popc(leads & ((1u << (lane_id & ~3u)) - 1u));
+    if (any && in && slot < cap) {
+      if (part == 0) idx[slot] = ((u64)r << 48) | cc;
+      pay[slot * 4 + part] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_delta_apply(RegionTab t, u64 n, const u64* idx, const uint4* pay) {
+  for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q < n * 4; q += (u64)gridDim.x * blockDim.x) {
+    const u64 j = q >> 2;
+    const u32 part = (u32)(q & 3);
+    const u64 e = idx[j];
+    const int r = (int)(e >> 48);
+    const u64 w = (e & ((1ull << 48) - 1)) * kChunkWords + part * 4;
+    const u64 words = t.words[r];
+    const uint4 v = pay[q];
+    if (w + 4 <= words) {
+      *(uint4*)(t.cur[r] + w) = v;
+    } else {
+      const u32 vv[4] = {v.x, v.y, v.z, v.w};
+      for (u64 k = 0; k < 4 && w + k < words; ++k) t.cur[r][w + k] = vv[k];
+    }
+  }
+}
+
+// Order-independent digest of a region's live words (tests: replica == rank 0).
+__global__ void k_digest(const u32* p, u64 words, unsigned long long* out) {
+  u64 acc = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (u64)gridDim.x * blockDim.x)
+    acc += mix64((i << 32) ^ (u64)p[i]);
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
+}
+
+// Match summaries: K1's per-request results as rows [S, dslot, dm, hints].
+__global__ void k_shard_pack(i64 lo, i64 cnt, const i64* S, const u32* dslot, const u32* dm, const u32* path,
+                             int hstride, char* out, u64 row_bytes, const unsigned int* deepest) {
+  const i64 i = (i64)blockIdx.x;
+  if (i == 0 && threadIdx.x == 0) {
+    ((u64*)out)[0] = *deepest;
+    ((u64*)out)[1] = (u64)cnt;
+  }
+  if (i >= cnt) return;
+  char* row = out + 16 + (u64)i * row_bytes;
+  const i64 w = lo + i;
+  if (threadIdx.x == 0) {
+    *(i64*)row = S[w];
+    ((u32*)row)[2] = dslot[w];
+    ((u32*)row)[3] = dm[w];
+  }
+  const u32* src = path + (u64)w * hstride;
+  u32* dst = (u32*)(row + 16);
+  for (int k = threadIdx.x; k < hstride; k += blockDim.x) {
+    const u32 v = src[k];
+    dst[k] = v;
+    if (v == kNil) break;  // rows are kNil-terminated
+  }
+}
+
+__global__ void k_shard_unpack(int world, i64 per, i64 nb, const char* in, u64 row_bytes, u64 slice_bytes, i64* S,
+                               u32* dslot, u32* dm, u32* path, int hstride, unsigned int* deepest) {
+  const i64 i = (i64)blockIdx.x;  // batch row
+  if (i >= nb) return;
+  const i64 k = i / per, j = i - k * per;
+  const char* sl = in + (u64)k * slice_bytes;
+  if (j == 0 && threadIdx.x == 0) atomicMax(deepest, (unsigned int)((const u64*)sl)[0]);
+  const char* row = sl + 16 + (u64)j * row_bytes;
+  if (threadIdx.x == 0) {
+    S[i] = *(const i64*)row;
+    dslot[i] = ((const u32*)row)[2];
+    dm[i] = ((const u32*)row)[3];
+  }
+  const u32* src = (const u32*)(row + 16);
+  u32* dst = path + (u64)i * hstride;
+  for (int q = threadIdx.x; q < hstride; q += blockDim.x) {
+    const u32 v = src[q];
+    dst[q] = v;
+    if (v == kNil) break;
+  }
+}
+#endif
+
 }  // namespace
 
 // last error of calls without a handle (e2_create, e2_generate)
@@ -329,6 +484,58 @@ void e2_set_global_error(const char* m) { g_err = m; }
 // ---------------------------------------------------------------------------
 // handle
 // ---------------------------------------------------------------------------
+// A batched replay in progress (e2_replay, or the sharded replay's steps).
+struct ReplaySession {
+  bool active = false;
+  bool device_ptrs = false;
+  bool stopped = false;
+  i64 n = 0, B = 0, next_b0 = 0, cur_b = 0, done = 0;
+  i64 cb0 = 0, cnb = 0;  // the current batch
+  SerialArgs a;
+  e2_decision* out = nullptr;  // caller's buffers
+  e2_cost* costs = nullptr;
+  double* ratios = nullptr;
+  e2_decision* d_dec = nullptr;  // device-side buffers the kernels write
+  e2_cost* d_cost = nullptr;
+  double* d_rat = nullptr;
+  std::string fail;
+  int fail_code = 0;
+  int saved_stream_valid = 0;
+  void* saved_stream = nullptr;
+};
+
+// The delta a sharded replay's rank 0 sends after each batch.
+struct DeltaHdr {
+  u64 magic;
+  i64 n_chunks;
+  i64 done;
+  i32 fail_code;
+  i32 want_hstride;
+  u32 n_regions;
+  u32 pad;
+  u64 region_words[kMaxRegions];
+  char msg[256];
+  Hot hot;
+};
+constexpr u64 kDeltaMagic = 0x4532444c54413031ull;  // "E2DLTA01"
+constexpr size_t kDeltaHdrBytes = (sizeof(DeltaHdr) + 63) / 64 * 64;
+
+struct ShardState {
+  bool on = false;
+  int rank = 0, world = 1;
+  // rank 0: shadow copy of each region as the replicas hold it
+  std::vector<u32*> sh;
+  std::vector<u64> sh_words;
+  std::vector<const void*> sh_src;  // region pointer the shadow was taken from
+  // rank 0: the last delta (chunk list + payload), library-owned
+  u64* dl_idx = nullptr;
+  uint4* dl_pay = nullptr;
+  u64 dl_cap = 0;
+  unsigned long long* dl_count = nullptr;
+  DeltaHdr hdr;
+  i64 row_bytes = 0;
+};
+
 struct e2_handle {
   Dev d;
   Hot hot;
@@ -382,6 +589,8 @@ struct e2_handle {
   u32 nsets = 0;          // node-cache sets of the serial kernel
   size_t serial_smem = 0;  // its dynamic shared memory
   i64 req_cap = 0;         // d.req_tail capacity
+  ReplaySession rs;
+  ShardState sh;
   // profiling
   bool prof = false;
   e2_profile acc;
@@ -810,80 +1019,110 @@ void note_depth(e2_handle* h, u64 levels) {
   h->want_hstride = std::max(h->want_hstride, want);
 }
 
-// K1 + leader rounds for requests [base, base+n) of the arena index.
-// Produces h->b_L[0..n).
-void launch_match(e2_handle* h, i64 base, i64 n) {
-  if (n == 0) return;
-  reserve_batch(h, n);
+// K1 over requests [base+lo, base+lo+cnt) of the arena index; results land
+// in the batch arrays at [lo, lo+cnt).  Returns the deepest path seen when it
+// reached the hint stride (0 otherwise) via note_depth on the device path.
+void k1_slice(e2_handle* h, i64 base, i64 lo, i64 cnt) {
+  if (cnt <= 0) return;
   [[maybe_unused]] Dev& d = h->d;  // the host emulation's match reads the arena through it
 #if E2_DEVICE_BUILD
-  {
-    const i64 blocks = (n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock;
-    const unsigned grid = (unsigned)std::min<i64>(blocks, (i64)h->n_sm * kMatchBlocksPerSM);
-    h->acc.launches[E2_K_MATCH]++;
-    upload_dev(h);
-    dset(h->d_cnt + 2, 0, 8, h->stream);  // [2] deepest path, [3] work counter
-    Timed t(h, E2_K_MATCH);  // the kernel alone (roofline denominator)
-    k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot,
-                                                             h->b_dm, h->b_path, h->hstride, h->d_bytes,
-                                                             h->d_cnt + 2, h->d_cnt + 3);
-    CK(cudaGetLastError());
-  }
-  h->acc.match_requests += n;
-  if (n == 1) {
-    // single sequence: no intra-batch dependency
-    d2d(h->b_L, h->b_S, 8, h->stream);
-    dset(h->b_leader, 0xff, 8, h->stream);  // -1: no in-batch leader
-    return;
-  }
-  Timed t(h, E2_K_GROUP);
-  const u64 tsz = h->g_mask + 1;
-  const unsigned tg = (unsigned)((n + 255) / 256);
-  dset(h->g_tk, 0, tsz * 8, h->stream);
-  dset(h->g_tv, 0xff, tsz * 4, h->stream);
-  h->acc.launches[E2_K_GROUP]++;
-  k_group_init<<<tg, 256, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot, h->b_dm, h->b_state,
-                                          h->b_A, h->b_B, h->b_cand, h->b_L, h->g_tk, h->g_tv, h->g_mask,
-                                          h->b_leader);
+  const i64 blocks = (cnt + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock;
+  const unsigned grid = (unsigned)std::min<i64>(blocks, (i64)h->n_sm * kMatchBlocksPerSM);
+  h->acc.launches[E2_K_MATCH]++;
+  upload_dev(h);
+  dset(h->d_cnt + 2, 0, 8, h->stream);  // [2] deepest path, [3] work counter
+  Timed t(h, E2_K_MATCH);  // the kernel alone (roofline denominator)
+  k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(cnt, base + lo, h->r_off, h->r_len, h->b_S + lo,
+                                                           h->b_dslot + lo, h->b_dm + lo,
+                                                           h->b_path + lo * h->hstride, h->hstride, h->d_bytes,
+                                                           h->d_cnt + 2, h->d_cnt + 3);
   CK(cudaGetLastError());
-  for (int round = 0;; ++round) {
-    dset(h->d_cnt, 0, 8, h->stream);
-    h->acc.launches[E2_K_GROUP]++;
-    k_group_resolve<<<tg, 256, 0, h->stream>>>(n, round, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
-                                               h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_cnt, h->d_cnt + 1);
-    CK(cudaGetLastError());
-    unsigned int cnt[3];
-    d2h(cnt, h->d_cnt, 12, h->stream);
-    ssync(h->stream);
-    note_depth(h, cnt[2]);
-    if (cnt[1]) throw Fail(E2_ERR_ARG, "intra-batch grouping hash collision");
-    if (cnt[0] == 0) break;
-    dset(h->g_tk, 0, tsz * 8, h->stream);
-    dset(h->g_tv, 0xff, tsz * 4, h->stream);
-    unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
-    h->acc.launches[E2_K_GROUP]++;
-    k_group_round<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(
-        n, base, round + 1, h->r_off, h->r_len, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader, h->b_o,
-        h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_bytes + 1);
-    CK(cudaGetLastError());
-  }
 #else
-  // host emulation: the same per-request functions, sequentially
-  std::vector<i64> S(n);
-  std::vector<u32> ds(n), dm(n);
-  for (i64 w = 0; w < n; ++w) {
+  h->d_cnt[2] = 0;
+  for (i64 w = lo; w < lo + cnt; ++w) {
     const i64 r = base + w;
     g_dev_h = h->d;
     MatchRes m = match_one(d.tok + h->r_off[r], h->r_len[r], h->b_path + w * h->hstride, h->hstride);
-    S[w] = m.S;
     h->b_S[w] = m.S;
-    ds[w] = m.div_slot;
-    dm[w] = m.div_m;
+    h->b_dslot[w] = m.div_slot;
+    h->b_dm[w] = m.div_m;
     h->d_bytes[0] += (unsigned long long)m.bytes;
-    if (m.levels >= h->hstride) note_depth(h, (u64)m.levels);
+    if (m.levels >= h->hstride) h->d_cnt[2] = std::max<unsigned int>(h->d_cnt[2], (unsigned int)m.levels);
   }
-  h->acc.match_requests += n;
-  // leader rounds with std::map grouping (same recursion as the device)
+#endif
+  h->acc.match_requests += cnt;
+}
+
+// Leader rounds over the batch [0, n) (K1 results in b_S/b_dslot/b_dm):
+// produces b_L and b_leader.  `deepest`: K1's deepest path beyond the hint
+// stride (device: already in d_cnt[2]).
+void group_rounds(e2_handle* h, i64 base, i64 n) {
+  [[maybe_unused]] Dev& d = h->d;
+  if (n == 1) {
+    // single sequence: no intra-batch dependency
+#if !E2_DEVICE_BUILD
+    note_depth(h, h->d_cnt[2]);
+#endif
+    d2d(h->b_L, h->b_S, 8, h->stream);
+    dset(h->b_leader, 0xff, 8, h->stream);  // -1: no in-batch leader
+#if E2_DEVICE_BUILD
+    unsigned int c2 = 0;
+    d2h(&c2, h->d_cnt + 2, 4, h->stream);
+    ssync(h->stream);
+    note_depth(h, c2);
+#endif
+    return;
+  }
+#if E2_DEVICE_BUILD
+  Timed t(h, E2_K_GROUP);
+  const u64 tsz = h->g_mask + 1;
+  const unsigned tg = (unsigned)((n + 255) / 256);
+  // A 64-bit key collision between two different (divergence point, next
+  // token) pairs is detected by k_group_resolve; the grouping then restarts
+  // with a fresh salt (a new hash family), so a collision costs one retry.
+  for (int attempt = 0;; ++attempt) {
+    if (attempt == 8) throw Fail(E2_ERR_ARG, "intra-batch grouping: repeated hash collisions");
+    const int salt = attempt * 4096;
+    dset(h->g_tk, 0, tsz * 8, h->stream);
+    dset(h->g_tv, 0xff, tsz * 4, h->stream);
+    h->acc.launches[E2_K_GROUP]++;
+    k_group_init<<<tg, 256, 0, h->stream>>>(n, base, h->r_off, h->r_len, h->b_S, h->b_dslot, h->b_dm, h->b_state,
+                                            h->b_A, h->b_B, h->b_cand, h->b_L, h->g_tk, h->g_tv, h->g_mask,
+                                            h->b_leader, salt);
+    CK(cudaGetLastError());
+    bool collided = false;
+    for (int round = 0;; ++round) {
+      dset(h->d_cnt, 0, 8, h->stream);
+      h->acc.launches[E2_K_GROUP]++;
+      k_group_resolve<<<tg, 256, 0, h->stream>>>(n, round + salt, h->b_state, h->b_A, h->b_B, h->b_cand,
+                                                 h->b_leader, h->b_o, h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_cnt,
+                                                 h->d_cnt + 1);
+      CK(cudaGetLastError());
+      unsigned int cnt[3];
+      d2h(cnt, h->d_cnt, 12, h->stream);
+      ssync(h->stream);
+      note_depth(h, cnt[2]);
+      if (cnt[1]) {
+        collided = true;
+        h->acc.group_retries++;
+        break;
+      }
+      if (cnt[0] == 0) break;
+      dset(h->g_tk, 0, tsz * 8, h->stream);
+      dset(h->g_tv, 0xff, tsz * 4, h->stream);
+      unsigned grid = (unsigned)((n + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock);
+      h->acc.launches[E2_K_GROUP]++;
+      k_group_round<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(
+          n, base, round + 1 + salt, h->r_off, h->r_len, h->b_state, h->b_A, h->b_B, h->b_cand, h->b_leader,
+          h->b_o, h->b_L, h->g_tk, h->g_tv, h->g_mask, h->d_bytes + 1);
+      CK(cudaGetLastError());
+    }
+    if (!collided) break;
+  }
+#else
+  note_depth(h, h->d_cnt[2]);
+  // host emulation: the same recursion with std::map grouping
+  const i64* S = h->b_S;
   std::vector<i32> st(n);
   std::vector<u64> A(n), B(n);
   std::vector<i64> cand(n), leader(n, -1), o(n);
@@ -896,7 +1135,7 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
       continue;
     }
     st[i] = 1;
-    A[i] = ((u64)ds[i] << 32) | dm[i];
+    A[i] = ((u64)h->b_dslot[i] << 32) | h->b_dm[i];
     B[i] = (u64)(u32)d.tok[h->r_off[r] + S[i]];
     cand[i] = S[i];
   }
@@ -937,6 +1176,15 @@ void launch_match(e2_handle* h, i64 base, i64 n) {
 #endif
 }
 
+// K1 + leader rounds for requests [base, base+n) of the arena index.
+// Produces h->b_L[0..n).
+void launch_match(e2_handle* h, i64 base, i64 n) {
+  if (n == 0) return;
+  reserve_batch(h, n);
+  k1_slice(h, base, 0, n);
+  group_rounds(h, base, n);
+}
+
 // Per-call API staging (pinned host memory).
 constexpr size_t kPinHead = (sizeof(Hot) + sizeof(ApiOut) + 63) / 64 * 64;
 
@@ -974,7 +1222,19 @@ void append_host_tokens(e2_handle* h, const i32* seq, i64 len) {
 
 
 // One API op on one sequence (or none): append, match, run.
-void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match) {
+// `transient`: the op stores no reference to the sequence (decide, match,
+// note_eviction: splits only cut existing edges), so its arena bytes are
+// handed back afterwards and read-only calls do not grow device memory.
+void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match, bool transient = false) {
+  const i64 tok_mark = h->tok_len;
+  struct Rollback {
+    e2_handle* h;
+    i64 mark;
+    bool on;
+    ~Rollback() {
+      if (on) h->tok_len = mark;
+    }
+  } rb{h, tok_mark, transient};
   reserve_for(h, 1, len);
   if (seq) {
     append_host_tokens(h, seq, len);
@@ -1024,6 +1284,16 @@ int guard(e2_handle* h, F&& f) {
     else g_err = e.what();
     return E2_ERR_ARG;
   }
+}
+
+// INT64_MIN marks an empty inflight slot (e2_state.cuh kNoInflight); the
+// reference's std::map accepts it, this implementation rejects it loudly.
+bool bad_id(e2_handle* h, int64_t id) {
+  if (id == kNoInflight) {
+    h->err = "request id INT64_MIN is reserved";
+    return true;
+  }
+  return false;
 }
 
 bool bad_gpu(e2_handle* h, int32_t g) {
@@ -1114,6 +1384,30 @@ double host_prefill_time(const e2_time_model& m, i64 missed) {
   return b;
 }
 
+// The subtree ops collect their nodes into vic_slot: size it from the host copy.
+u64 subtree_size(const HostTree& t, u32 n) {
+  u64 c = 0;
+  std::vector<u32> st{n};
+  while (!st.empty()) {
+    const u32 x = st.back();
+    st.pop_back();
+    ++c;
+    for (u32 y : t.kids[x]) st.push_back(y);
+  }
+  return c;
+}
+void reserve_victims(e2_handle* h, u64 need) {
+  Dev& d = h->d;
+  if (need <= d.vcap) return;
+  const u64 cap = pow2_at_least(need);
+  if (cap > 0xffffffffull) throw Fail(E2_ERR_ARG, "victim scratch exceeds 32-bit indices");
+  dfree(d.vic_slot);
+  dfree(d.vic_tok);
+  d.vic_slot = talloc<u32>(cap);
+  d.vic_tok = talloc<i64>(cap);
+  d.vcap = (u32)cap;
+}
+
 void replicate_prefix(e2_handle* h, u32 root_child, int target, double now) {
   run_simple(h, OP_MARK_NODE, target, root_child, now);
   run_simple(h, OP_EXPIRE_ALL, 0, 0, now);  // windowed hits for all instances
@@ -1162,6 +1456,7 @@ void replicate_prefix(e2_handle* h, u32 root_child, int target, double now) {
       owners |= t.cmask[x];
       for (u32 y : t.kids[x]) st.push_back(y);
     }
+    reserve_victims(h, subtree_size(t, n));
     run_simple(h, OP_MARK_SUBTREE, target, n, now);
     for (int g = 0; g < G; ++g)
       if (((owners >> g) & 1ull) && g != target) run_simple(h, OP_UNCACHE_SUBTREE, g, n, now);
@@ -1278,6 +1573,7 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     return E2_ERR_ARG;
   }
   e2_handle* h = new e2_handle();
+  memset(&h->d, 0, sizeof(h->d));  // every device pointer null until allocated (teardown on failure)
   int rc = guard(nullptr, [&] {
     h->G = n_gpus;
     h->cfg = *cfg;
@@ -1365,15 +1661,20 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
   });
   if (rc != E2_OK) {
     if (g_err.empty()) g_err = h->err;
-    delete h;
+    e2_destroy(h);  // frees what was allocated before the failure, and the stream
     return rc;
   }
   *out = h;
   return E2_OK;
 }
 
+namespace {
+void shadow_free(e2_handle* h);  // (sharded replay, below)
+}
+
 void e2_destroy(e2_handle* h) {
   if (!h) return;
+  shadow_free(h);
   Dev& d = h->d;
   void* ptrs[] = {d.rec, d.ct, d.win, d.comp, d.plog, d.dir, d.pg_la, d.pg_id, d.pg_slot, d.free_pages, d.inf, d.fifo_req,
                   d.fifo_tail, d.req_tail, d.scr_slot, d.scr_val, d.scr_la, d.scr_id, d.vic_slot, d.vic_tok, d.hot_g,
@@ -1448,6 +1749,7 @@ int e2_set_stream(e2_handle* h, void* stream) {
 
 int e2_schedule(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t request_id, double arrival_ms,
                 double now, e2_decision* out, e2_cost* costs, double* ratios) {
+  if (bad_id(h, request_id)) return E2_ERR_ARG;
   return guard(h, [&] {
     OpDesc op;
     memset(&op, 0, sizeof(op));
@@ -1471,12 +1773,13 @@ int e2_decide(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t r
     op.id = request_id;
     op.now = now;
     static const i32 dummy = 0;
-    run_api(h, op, prompt_len ? prompt : &dummy, prompt_len, true);
+    run_api(h, op, prompt_len ? prompt : &dummy, prompt_len, true, true);
     copy_decision(h, out, costs, ratios);
   });
 }
 
 int e2_note_admitted(e2_handle* h, int64_t request_id, double now) {
+  if (bad_id(h, request_id)) return E2_ERR_ARG;
   return guard(h, [&] {
     if (h->pol.mode != E2_MODE_PREFIX_AWARE) return;
     OpDesc op;
@@ -1515,11 +1818,12 @@ int e2_note_eviction(e2_handle* h, const int32_t* seq, int64_t seq_len, int64_t 
     op.gpu = gpu;
     op.x = tail_len;
     op.now = now;
-    run_api(h, op, seq, seq_len, true);
+    run_api(h, op, seq, seq_len, true, true);
   });
 }
 
 int e2_note_finished(e2_handle* h, int64_t request_id, double now, int64_t output_len) {
+  if (bad_id(h, request_id)) return E2_ERR_ARG;
   return guard(h, [&] {
     OpDesc op;
     memset(&op, 0, sizeof(op));
@@ -1613,7 +1917,7 @@ int e2_match(e2_handle* h, const int32_t* seq, int64_t len, int64_t* matched_len
     memset(&op, 0, sizeof(op));
     op.kind = OP_MATCH;
     static const i32 dummy = 0;
-    run_api(h, op, len ? seq : &dummy, len, true);
+    run_api(h, op, len ? seq : &dummy, len, true, true);
     if (matched_len) *matched_len = h->api.i0;
     if (cached_len) *cached_len = h->api.i1;
     if (per_gpu)
@@ -1740,166 +2044,411 @@ int e2_debug_dump(e2_handle* h, double now, char* buf, size_t cap, size_t* neede
 }
 
 // ---- batched replay ---------------------------------------------------------
+// One replay is begin / (next, match, commit)* / end.  e2_replay runs the
+// steps back to back; the sharded replay (e2_shard_*) runs the same steps
+// with K1 split across ranks and rank 0's state shipped as a delta.
 namespace {
+void replay_begin(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const int64_t* ids,
+                  const double* arrivals, const int64_t* output_lens, int64_t n, const e2_driver_cfg* drv,
+                  e2_decision* out, e2_cost* costs, double* ratios, bool device_ptrs) {
+  if (!h->queue_stats.empty() && h->pol.autoscale && h->pol.mode == E2_MODE_PREFIX_AWARE)
+    throw Fail(E2_ERR_ARG, "replay with pending autoscale queue statistics is not supported");
+  ReplaySession& S = h->rs;
+  S = ReplaySession();
+  S.n = n;
+  S.device_ptrs = device_ptrs;
+  S.out = out;
+  S.costs = costs;
+  S.ratios = ratios;
+  if (n <= 0) {
+    S.active = true;
+    return;
+  }
+  const int G = h->G;
+  i64 off0 = 0, offn = 0;
+  if (device_ptrs) {
+    d2h(&off0, offsets, 8, h->stream);
+    d2h(&offn, offsets + n, 8, h->stream);
+    ssync(h->stream);
+  } else {
+    off0 = offsets[0];
+    offn = offsets[n];
+    for (i64 i = 0; i < n; ++i)
+      if (ids[i] == kNoInflight) throw Fail(E2_ERR_ARG, "request id INT64_MIN is reserved");
+  }
+  const i64 ntok = offn - off0;
+  reserve_for(h, n, ntok);
+  reserve_requests(h, n);
+  // token arena: append the trace
+  const i64 base_tok = h->tok_len;
+  const i64 pad = (4 - (base_tok & 3)) & 3;  // 16-byte align the trace start
+  reserve_tokens(h, base_tok + pad + ntok);
+  const i64 tstart = base_tok + pad;
+  if (device_ptrs)
+    d2d(h->tok + tstart, tokens + off0, (size_t)ntok * 4, h->stream);
+  else
+    h2d(h->tok + tstart, tokens + off0, (size_t)ntok * 4, h->stream);
+  h->tok_len = tstart + ntok;
+  // per-request arrays resident on the device
+  i64 *d_ids = nullptr, *d_out = nullptr, *d_offs = nullptr;
+  double* d_arr = nullptr;
+  if (device_ptrs) {
+    d_ids = (i64*)ids;
+    d_arr = (double*)arrivals;
+    d_out = (i64*)output_lens;
+    d_offs = (i64*)offsets;
+    S.d_dec = out;
+    S.d_cost = costs;
+    S.d_rat = ratios;
+  } else {
+    if (n > h->st_cap) {
+      for (void* p : {(void*)h->st_ids, (void*)h->st_out, (void*)h->st_offs, (void*)h->st_arr, (void*)h->st_dec}) dfree(p);
+      h->st_ids = talloc<i64>(n);
+      h->st_arr = talloc<double>(n);
+      h->st_out = talloc<i64>(n);
+      h->st_offs = talloc<i64>(n + 1);
+      h->st_dec = talloc<e2_decision>(n);
+      h->st_cap = n;
+    }
+    if (costs && n * (G + 1) > h->st_cost_cap) {
+      dfree(h->st_cost);
+      h->st_cost = talloc<e2_cost>((size_t)n * (G + 1));
+      h->st_cost_cap = n * (G + 1);
+    }
+    if (ratios && n * G > h->st_rat_cap) {
+      dfree(h->st_rat);
+      h->st_rat = talloc<double>((size_t)n * G);
+      h->st_rat_cap = n * G;
+    }
+    d_ids = h->st_ids;
+    d_arr = h->st_arr;
+    d_out = h->st_out;
+    d_offs = h->st_offs;
+    S.d_dec = h->st_dec;
+    S.d_cost = costs ? h->st_cost : nullptr;
+    S.d_rat = ratios ? h->st_rat : nullptr;
+    h2d(d_ids, ids, n * 8, h->stream);
+    h2d(d_arr, arrivals, n * 8, h->stream);
+    h2d(d_out, output_lens, n * 8, h->stream);
+    h2d(d_offs, offsets, (n + 1) * 8, h->stream);
+  }
+#if E2_DEVICE_BUILD
+  {
+    Timed t(h, E2_K_OTHER);
+    h->acc.launches[E2_K_OTHER]++;
+    k_arena_index<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(n, tstart, d_offs, h->r_off, h->r_len, 0);
+    CK(cudaGetLastError());
+  }
+#else
+  for (i64 i = 0; i < n; ++i) {
+    h->r_off[i] = tstart + d_offs[i] - d_offs[0];
+    h->r_len[i] = d_offs[i + 1] - d_offs[i];
+  }
+#endif
+  // driver state
+  h->hot.drv_now = 0;
+  for (int g = 0; g < G; ++g) h->hot.fifo_head[g] = h->hot.fifo_tail[g] = 0;
+  push_hot(h);
+  S.B = drv->batch > 0 ? drv->batch : 16384;
+  reserve_batch(h, std::min<i64>(S.B, n));
+  if (n > h->req_cap) {
+    dfree(h->d.req_tail);
+    h->d.req_tail = talloc<u32>(n);
+    h->req_cap = n;
+  }
+  SerialArgs& a = S.a;
+  memset(&a, 0, sizeof(a));
+  a.kind = 0;
+  a.eviction = drv->eviction;
+  a.prefill = drv->prefill_cached;
+  a.off = h->r_off;
+  a.len = h->r_len;
+  a.ids = d_ids;
+  a.arr = d_arr;
+  a.outl = d_out;
+  a.L = h->b_L;
+  a.S = h->b_S;
+  a.lead = h->b_leader;
+  a.hint = h->b_path;
+  a.dec = S.d_dec;
+  a.costs = S.d_cost;
+  a.ratios = S.d_rat;
+  a.trunk = drv->trunk_len;
+  a.hw = drv->high_water;
+  a.lag = drv->finish_lag;
+  // Batch sizes ramp up geometrically from kFirstBatch: a batch is matched
+  // against the tree at its start, so early batches (a cold tree) would
+  // leave most requests without K1 path hints.
+  S.cur_b = std::min<i64>(S.B, n <= 4 * kFirstBatch ? kShortFirstBatch : kFirstBatch);
+  S.next_b0 = 0;
+  S.active = true;
+}
+
+// The next batch [cb0, cb0+cnb); false when the replay is complete or stopped.
+bool replay_next(e2_handle* h) {
+  ReplaySession& S = h->rs;
+  if (!S.active) throw Fail(E2_ERR_ARG, "no replay in progress");
+  if (S.stopped || S.next_b0 >= S.n) {
+    S.cnb = 0;
+    return false;
+  }
+  S.cb0 = S.next_b0;
+  S.cnb = std::min<i64>(S.cur_b, S.n - S.next_b0);
+  S.next_b0 += S.cur_b;
+  S.cur_b = std::min<i64>(S.B, S.cur_b * 2);
+  reserve_batch(h, S.cnb);
+  return true;
+}
+
+// The serial decide/commit pass over the current batch (K1 + leader rounds done).
+void replay_commit(e2_handle* h) {
+  ReplaySession& S = h->rs;
+  SerialArgs& a = S.a;
+  a.L = h->b_L;
+  a.S = h->b_S;
+  a.lead = h->b_leader;
+  a.hint = h->b_path;  // the hint stride may have grown
+  a.hstride = h->hstride;
+  a.base = S.cb0;
+  a.n = S.cnb;
+  launch_serial(h, a);
+  pull_hot(h);
+  S.done = S.cb0 + h->hot.done;
+  if (h->hot.err) {
+    try {
+      check_hot_error(h);
+    } catch (const Fail& e) {
+      S.fail = e.what();
+      S.fail_code = e.code;
+    }
+    S.stopped = true;
+  }
+}
+
+void replay_after_batch(e2_handle* h) {
+  if (!h->rs.stopped) reserve_plog(h);
+}
+
+void replay_end(e2_handle* h, int64_t* n_done) {
+  ReplaySession& S = h->rs;
+  if (!S.active) throw Fail(E2_ERR_ARG, "no replay in progress");
+  S.active = false;
+  prof_flush(h);
+  const i64 done = S.done;
+  if (!S.device_ptrs && done > 0) {
+    const int G = h->G;
+    d2h(S.out, S.d_dec, (size_t)done * sizeof(e2_decision), h->stream);
+    if (S.costs) d2h(S.costs, S.d_cost, (size_t)done * (G + 1) * sizeof(e2_cost), h->stream);
+    if (S.ratios) d2h(S.ratios, S.d_rat, (size_t)done * G * 8, h->stream);
+    ssync(h->stream);
+  }
+  if (n_done) *n_done = done;
+  if (S.fail_code) throw Fail(S.fail_code, S.fail + " (request index " + std::to_string(done) + ")");
+}
+
 int replay_impl(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const int64_t* ids,
                 const double* arrivals, const int64_t* output_lens, int64_t n, const e2_driver_cfg* drv,
                 e2_decision* out, e2_cost* costs, double* ratios, int64_t* n_done, bool device_ptrs) {
   if (n_done) *n_done = 0;
   return guard(h, [&] {
     if (n <= 0) return;
-    if (!h->queue_stats.empty() && h->pol.autoscale && h->pol.mode == E2_MODE_PREFIX_AWARE)
-      throw Fail(E2_ERR_ARG, "replay with pending autoscale queue statistics is not supported");
-    const int G = h->G;
-    i64 off0 = 0, offn = 0;
-    if (device_ptrs) {
-      d2h(&off0, offsets, 8, h->stream);
-      d2h(&offn, offsets + n, 8, h->stream);
-      ssync(h->stream);
-    } else {
-      off0 = offsets[0];
-      offn = offsets[n];
+    replay_begin(h, tokens, offsets, ids, arrivals, output_lens, n, drv, out, costs, ratios, device_ptrs);
+    try {
+      while (replay_next(h)) {
+        launch_match(h, h->rs.cb0, h->rs.cnb);
+        replay_commit(h);
+        replay_after_batch(h);
+      }
+    } catch (...) {
+      h->rs.active = false;
+      throw;
     }
-    const i64 ntok = offn - off0;
-    reserve_for(h, n, ntok);
-    reserve_requests(h, n);
-    // token arena: append the trace
-    const i64 base_tok = h->tok_len;
-    const i64 pad = (4 - (base_tok & 3)) & 3;  // 16-byte align the trace start
-    reserve_tokens(h, base_tok + pad + ntok);
-    const i64 tstart = base_tok + pad;
-    if (device_ptrs)
-      d2d(h->tok + tstart, tokens + off0, (size_t)ntok * 4, h->stream);
-    else
-      h2d(h->tok + tstart, tokens + off0, (size_t)ntok * 4, h->stream);
-    h->tok_len = tstart + ntok;
-    // per-request arrays resident on the device
-    i64 *d_ids = nullptr, *d_out = nullptr, *d_offs = nullptr;
-    double* d_arr = nullptr;
-    e2_decision* d_dec = nullptr;
-    e2_cost* d_cost = nullptr;
-    double* d_rat = nullptr;
-    if (device_ptrs) {
-      d_ids = (i64*)ids;
-      d_arr = (double*)arrivals;
-      d_out = (i64*)output_lens;
-      d_offs = (i64*)offsets;
-      d_dec = out;
-      d_cost = costs;
-      d_rat = ratios;
-    } else {
-      if (n > h->st_cap) {
-        for (void* p : {(void*)h->st_ids, (void*)h->st_out, (void*)h->st_offs, (void*)h->st_arr, (void*)h->st_dec}) dfree(p);
-        h->st_ids = talloc<i64>(n);
-        h->st_arr = talloc<double>(n);
-        h->st_out = talloc<i64>(n);
-        h->st_offs = talloc<i64>(n + 1);
-        h->st_dec = talloc<e2_decision>(n);
-        h->st_cap = n;
-      }
-      if (costs && n * (G + 1) > h->st_cost_cap) {
-        dfree(h->st_cost);
-        h->st_cost = talloc<e2_cost>((size_t)n * (G + 1));
-        h->st_cost_cap = n * (G + 1);
-      }
-      if (ratios && n * G > h->st_rat_cap) {
-        dfree(h->st_rat);
-        h->st_rat = talloc<double>((size_t)n * G);
-        h->st_rat_cap = n * G;
-      }
-      d_ids = h->st_ids;
-      d_arr = h->st_arr;
-      d_out = h->st_out;
-      d_offs = h->st_offs;
-      d_dec = h->st_dec;
-      d_cost = costs ? h->st_cost : nullptr;
-      d_rat = ratios ? h->st_rat : nullptr;
-      h2d(d_ids, ids, n * 8, h->stream);
-      h2d(d_arr, arrivals, n * 8, h->stream);
-      h2d(d_out, output_lens, n * 8, h->stream);
-      h2d(d_offs, offsets, (n + 1) * 8, h->stream);
-    }
+    replay_end(h, n_done);
+  });
+}
+
+// ---- sharded replay: regions, delta export/apply ---------------------------
+RegionTab state_regions(e2_handle* h) {
+  Dev& d = h->d;
+  const u64 G = (u64)h->G;
+  RegionTab t;
+  memset(&t, 0, sizeof(t));
+  auto add = [&](void* p, u64 bytes) {
+    t.cur[t.n] = (u32*)p;
+    t.words[t.n] = p ? bytes / 4 : 0;
+    t.live_words[t.n] = t.words[t.n];
+    t.n++;
+  };
+  add(d.rec, (u64)d.node_cap * d.rs);
+  add(d.ct, (d.ct_mask + 1) * sizeof(CtEntry));
+  add(d.win, d.wcap * G * sizeof(WinEnt));
+  add(d.comp, d.wcap * G * sizeof(CompEnt));
+  add(d.plog, d.pcap * G * 4);
+  add(d.dir, (u64)d.dcap * G * sizeof(DirEntry));
+  add(d.pg_la, (u64)d.page_cap * kPage * 8);
+  add(d.pg_id, (u64)d.page_cap * kPage * 8);
+  add(d.pg_slot, (u64)d.page_cap * kPage * 4);
+  add(d.free_pages, (u64)d.page_cap * 4);
+  add(d.inf, (d.inf_mask + 1) * sizeof(InfRec));
+  add(d.fifo_req, d.fcap * G * 8);
+  add(d.fifo_tail, d.fcap * G * 8);
+  add(d.req_tail, (u64)h->req_cap * 4);
+  // only the used part of the node pool can have changed
+  t.live_words[0] = std::min<u64>(t.words[0], (u64)h->hot.slots_used * d.rs / 4);
+  return t;
+}
+
+// (Re)take rank 0's shadow of every region whose allocation changed since
+// the last snapshot (all of them on the first call).
+void shadow_sync(e2_handle* h) {
+  ShardState& sh = h->sh;
+  RegionTab t = state_regions(h);
+  if ((int)sh.sh.size() != t.n) {
+    sh.sh.assign(t.n, nullptr);
+    sh.sh_words.assign(t.n, 0);
+    sh.sh_src.assign(t.n, nullptr);
+  }
+  for (int r = 0; r < t.n; ++r) {
+    if (sh.sh_src[r] == t.cur[r] && sh.sh_words[r] == t.words[r]) continue;
+    dfree(sh.sh[r]);
+    sh.sh[r] = talloc<u32>(std::max<u64>(t.words[r], 1));
+    if (t.words[r]) d2d(sh.sh[r], t.cur[r], t.words[r] * 4, h->stream);
+    sh.sh_words[r] = t.words[r];
+    sh.sh_src[r] = t.cur[r];
+  }
+  ssync(h->stream);
+}
+
+void shadow_free(e2_handle* h) {
+  ShardState& sh = h->sh;
+  for (u32* p : sh.sh) dfree(p);
+  sh.sh.clear();
+  sh.sh_words.clear();
+  sh.sh_src.clear();
+  dfree(sh.dl_idx);
+  dfree(sh.dl_pay);
+  dfree(sh.dl_count);
+  sh.dl_idx = nullptr;
+  sh.dl_pay = nullptr;
+  sh.dl_count = nullptr;
+  sh.dl_cap = 0;
+}
+
+// Apply n chunks (idx/payload) to the regions of `t` (cur pointers).
+void delta_apply(e2_handle* h, const RegionTab& t, u64 n, const u64* idx, const uint4* pay) {
+  if (!n) return;
 #if E2_DEVICE_BUILD
-    {
-      Timed t(h, E2_K_OTHER);
-      h->acc.launches[E2_K_OTHER]++;
-      k_arena_index<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(n, tstart, d_offs, h->r_off, h->r_len, 0);
+  const u64 q = n * 4;
+  const unsigned grid = (unsigned)std::min<u64>((q + 255) / 256, (u64)h->n_sm * 8);
+  k_delta_apply<<<grid, 256, 0, h->stream>>>(t, n, idx, pay);
+  CK(cudaGetLastError());
+#else
+  (void)h;
+  for (u64 j = 0; j < n; ++j) {
+    const int r = (int)(idx[j] >> 48);
+    const u64 w0 = (idx[j] & ((1ull << 48) - 1)) * kChunkWords;
+    const u32* src = (const u32*)&pay[j * 4];
+    for (u64 k = 0; k < kChunkWords && w0 + k < t.words[r]; ++k) t.cur[r][w0 + k] = src[k];
+  }
+#endif
+}
+
+// Rank 0, after a committed batch: diff the regions against the shadow into
+// dl_idx/dl_pay, fill the header, apply the chunks to the shadow.
+void delta_export(e2_handle* h) {
+  ShardState& sh = h->sh;
+  RegionTab t = state_regions(h);
+  if ((int)sh.sh.size() != t.n) throw Fail(E2_ERR_ARG, "shard: shadow not initialised");
+  u64 total = 0;
+  for (int r = 0; r < t.n; ++r) {
+    if (sh.sh_src[r] != t.cur[r] || sh.sh_words[r] != t.words[r])
+      throw Fail(E2_ERR_ARG, "shard: a region moved inside a batch");
+    t.sh[r] = sh.sh[r];
+    t.chunk0[r] = total;
+    total += (t.live_words[r] + kChunkWords - 1) / kChunkWords;
+  }
+  t.chunk0[t.n] = total;
+  u64 n = 0;
+#if E2_DEVICE_BUILD
+  if (!sh.dl_count) sh.dl_count = talloc<unsigned long long>(1);
+  for (int pass = 0; pass < 2; ++pass) {
+    if (!sh.dl_idx) {
+      sh.dl_cap = std::max<u64>(sh.dl_cap, 1 << 16);
+      sh.dl_idx = talloc<u64>(sh.dl_cap);
+      sh.dl_pay = talloc<uint4>(sh.dl_cap * 4);
+    }
+    dset(sh.dl_count, 0, 8, h->stream);
+    const u64 quads = total * 4;
+    if (quads) {
+      const unsigned grid = (unsigned)std::min<u64>((quads + 255) / 256, (u64)h->n_sm * 8);
+      k_delta_diff<<<grid, 256, 0, h->stream>>>(t, quads, sh.dl_idx, sh.dl_pay, sh.dl_cap, sh.dl_count);
       CK(cudaGetLastError());
     }
+    unsigned long long c = 0;
+    d2h(&c, sh.dl_count, 8, h->stream);
+    ssync(h->stream);
+    n = c;
+    if (n <= sh.dl_cap) break;
+    dfree(sh.dl_idx);
+    dfree(sh.dl_pay);
+    sh.dl_idx = nullptr;
+    sh.dl_cap = n + n / 4;
+  }
 #else
-    for (i64 i = 0; i < n; ++i) {
-      h->r_off[i] = tstart + d_offs[i] - d_offs[0];
-      h->r_len[i] = d_offs[i + 1] - d_offs[i];
+  std::vector<u64> idx;
+  std::vector<uint4> pay;
+  for (int r = 0; r < t.n; ++r) {
+    const u64 lw = t.live_words[r];
+    for (u64 c = 0; c * kChunkWords < lw; ++c) {
+      const u64 w0 = c * kChunkWords;
+      bool diff = false;
+      for (u64 k = 0; k < kChunkWords && w0 + k < lw; ++k) diff |= t.cur[r][w0 + k] != t.sh[r][w0 + k];
+      if (!diff) continue;
+      idx.push_back(((u64)r << 48) | c);
+      u32 v[kChunkWords] = {0};
+      for (u64 k = 0; k < kChunkWords && w0 + k < lw; ++k) v[k] = t.cur[r][w0 + k];
+      for (int q = 0; q < 4; ++q) pay.push_back(uint4{v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]});
     }
+  }
+  n = idx.size();
+  if (n > sh.dl_cap) {
+    dfree(sh.dl_idx);
+    dfree(sh.dl_pay);
+    sh.dl_cap = n + n / 4 + 16;
+    sh.dl_idx = talloc<u64>(sh.dl_cap);
+    sh.dl_pay = talloc<uint4>(sh.dl_cap * 4);
+  }
+  if (n) {
+    memcpy(sh.dl_idx, idx.data(), n * 8);
+    memcpy(sh.dl_pay, pay.data(), n * 64);
+  }
 #endif
-    // driver state
-    h->hot.drv_now = 0;
-    for (int g = 0; g < G; ++g) h->hot.fifo_head[g] = h->hot.fifo_tail[g] = 0;
-    push_hot(h);
-    const i64 B = drv->batch > 0 ? drv->batch : 16384;
-    reserve_batch(h, std::min<i64>(B, n));
-    if (n > h->req_cap) {
-      dfree(h->d.req_tail);
-      h->d.req_tail = talloc<u32>(n);
-      h->req_cap = n;
-    }
-    SerialArgs a;
-    memset(&a, 0, sizeof(a));
-    a.kind = 0;
-    a.eviction = drv->eviction;
-    a.prefill = drv->prefill_cached;
-    a.off = h->r_off;
-    a.len = h->r_len;
-    a.ids = d_ids;
-    a.arr = d_arr;
-    a.outl = d_out;
-    a.L = h->b_L;
-    a.S = h->b_S;
-    a.lead = h->b_leader;
-    a.hint = h->b_path;
-    a.dec = d_dec;
-    a.costs = d_cost;
-    a.ratios = d_rat;
-    a.trunk = drv->trunk_len;
-    a.hw = drv->high_water;
-    a.lag = drv->finish_lag;
-    i64 done = 0;
-    std::string fail;
-    int fail_code = 0;
-    // Batch sizes ramp up geometrically from kFirstBatch: a batch is matched
-    // against the tree at its start, so early batches (a cold tree) would
-    // leave most requests without K1 path hints.
-    i64 cur_b = std::min<i64>(B, n <= 4 * kFirstBatch ? kShortFirstBatch : kFirstBatch);
-    for (i64 b0 = 0; b0 < n; b0 += cur_b, cur_b = std::min<i64>(B, cur_b * 2)) {
-      const i64 nb = std::min<i64>(cur_b, n - b0);
-      launch_match(h, b0, nb);
-      a.hint = h->b_path;  // the hint stride may have grown
-      a.hstride = h->hstride;
-      a.base = b0;
-      a.n = nb;
-      launch_serial(h, a);
-      pull_hot(h);
-      done = b0 + h->hot.done;
-      if (h->hot.err) {
-        try {
-          check_hot_error(h);
-        } catch (const Fail& e) {
-          fail = e.what();
-          fail_code = e.code;
-        }
-        break;
-      }
-      reserve_plog(h);
-    }
-    prof_flush(h);
-    if (!device_ptrs) {
-      d2h(out, d_dec, (size_t)done * sizeof(e2_decision), h->stream);
-      if (costs) d2h(costs, d_cost, (size_t)done * (G + 1) * sizeof(e2_cost), h->stream);
-      if (ratios) d2h(ratios, d_rat, (size_t)done * G * 8, h->stream);
-      ssync(h->stream);
-    }
-    if (n_done) *n_done = done;
-    if (fail_code) throw Fail(fail_code, fail + " (request index " + std::to_string(done) + ")");
-  });
+  // the replicas will hold exactly this: bring the shadow along
+  RegionTab ts = t;
+  for (int r = 0; r < t.n; ++r) ts.cur[r] = sh.sh[r];
+  delta_apply(h, ts, n, sh.dl_idx, sh.dl_pay);
+  DeltaHdr& hd = sh.hdr;
+  memset(&hd, 0, sizeof(hd));
+  hd.magic = kDeltaMagic;
+  hd.n_chunks = (i64)n;
+  hd.done = h->rs.done;
+  hd.fail_code = h->rs.fail_code;
+  hd.want_hstride = h->want_hstride;
+  hd.n_regions = (u32)t.n;
+  for (int r = 0; r < t.n; ++r) hd.region_words[r] = t.words[r];
+  snprintf(hd.msg, sizeof(hd.msg), "%s", h->rs.fail.c_str());
+  hd.hot = h->hot;
+  h->acc.delta_chunks += (i64)n;
+  h->acc.delta_bytes += (i64)(kDeltaHdrBytes + n * 8 + n * 64);
+  ssync(h->stream);
+}
+
+u64 delta_bytes_of(u64 n) { return kDeltaHdrBytes + (n * 8 + 63) / 64 * 64 + n * 64; }
+
+void shard_check(e2_handle* h, bool rank0) {
+  if (!h->sh.on || !h->rs.active) throw Fail(E2_ERR_ARG, "no sharded replay in progress");
+  if (rank0 && h->sh.rank != 0) throw Fail(E2_ERR_ARG, "this step runs on rank 0 only");
+  if (!rank0 && h->sh.rank == 0) throw Fail(E2_ERR_ARG, "this step runs on the replicas only");
 }
 }  // namespace
 
@@ -1924,6 +2473,193 @@ int e2_replay_device(e2_handle* h, const int32_t* d_tokens, const int64_t* d_off
   return replay_impl(h, d_tokens, d_offsets, d_ids, d_arrivals, d_output_lens, n, drv, d_out, d_costs, d_ratios,
                      n_done, true);
 #endif
+}
+
+// ---- sharded replay ------------------------------------------
+int e2_shard_begin(e2_handle* h, const int32_t* d_tokens, const int64_t* d_offsets, const int64_t* d_ids,
+                   const double* d_arrivals, const int64_t* d_output_lens, int64_t n, const e2_driver_cfg* drv,
+                   e2_decision* d_out, e2_cost* d_costs, double* d_ratios, int32_t rank, int32_t world) {
+  return guard(h, [&] {
+    if (world < 1 || rank < 0 || rank >= world) throw Fail(E2_ERR_ARG, "shard: bad rank/world");
+    if (n <= 0) throw Fail(E2_ERR_ARG, "shard: empty trace");
+    h->sh.on = true;
+    h->sh.rank = rank;
+    h->sh.world = world;
+    replay_begin(h, d_tokens, d_offsets, d_ids, d_arrivals, d_output_lens, n, drv, rank == 0 ? d_out : nullptr,
+                 rank == 0 ? d_costs : nullptr, rank == 0 ? d_ratios : nullptr, true);
+    if (rank == 0) shadow_sync(h);
+  });
+}
+
+int e2_shard_next(e2_handle* h, int64_t* b0, int64_t* nb, int64_t* row_bytes) {
+  return guard(h, [&] {
+    if (!h->sh.on) throw Fail(E2_ERR_ARG, "no sharded replay in progress");
+    const bool more = replay_next(h);
+    *b0 = h->rs.cb0;
+    *nb = more ? h->rs.cnb : 0;
+    h->sh.row_bytes = 16 + 4 * (i64)h->hstride;
+    *row_bytes = h->sh.row_bytes;
+  });
+}
+
+int e2_shard_match(e2_handle* h, int64_t lo, int64_t cnt, void* d_slice) {
+  return guard(h, [&] {
+    if (!h->sh.on || !h->rs.active) throw Fail(E2_ERR_ARG, "no sharded replay in progress");
+    if (lo < 0 || cnt < 0 || lo + cnt > h->rs.cnb) throw Fail(E2_ERR_ARG, "shard: slice outside the batch");
+    const u64 rb = (u64)h->sh.row_bytes;
+#if E2_DEVICE_BUILD
+    if (cnt > 0) {
+      k1_slice(h, h->rs.cb0, lo, cnt);
+    } else {
+      dset(h->d_cnt + 2, 0, 4, h->stream);
+    }
+    k_shard_pack<<<(unsigned)std::max<i64>(cnt, 1), 128, 0, h->stream>>>(lo, cnt, h->b_S, h->b_dslot, h->b_dm,
+                                                                         h->b_path, h->hstride, (char*)d_slice, rb,
+                                                                         h->d_cnt + 2);
+    CK(cudaGetLastError());
+    ssync(h->stream);
+#else
+    h->d_cnt[2] = 0;
+    k1_slice(h, h->rs.cb0, lo, cnt);
+    char* out = (char*)d_slice;
+    ((u64*)out)[0] = h->d_cnt[2];
+    ((u64*)out)[1] = (u64)cnt;
+    for (i64 i = 0; i < cnt; ++i) {
+      char* row = out + 16 + (u64)i * rb;
+      const i64 w = lo + i;
+      *(i64*)row = h->b_S[w];
+      ((u32*)row)[2] = h->b_dslot[w];
+      ((u32*)row)[3] = h->b_dm[w];
+      memcpy(row + 16, h->b_path + (u64)w * h->hstride, (size_t)h->hstride * 4);
+    }
+#endif
+  });
+}
+
+int e2_shard_commit(e2_handle* h, const void* d_gathered, int64_t per, int64_t* delta_bytes) {
+  return guard(h, [&] {
+    shard_check(h, true);
+    const i64 nb = h->rs.cnb;
+    const int world = h->sh.world;
+    if (per * world < nb) throw Fail(E2_ERR_ARG, "shard: slices do not cover the batch");
+    const u64 rb = (u64)h->sh.row_bytes, slice = 16 + (u64)per * rb;
+#if E2_DEVICE_BUILD
+    dset(h->d_cnt + 2, 0, 4, h->stream);
+    if (nb > 0)
+      k_shard_unpack<<<(unsigned)nb, 128, 0, h->stream>>>(world, per, nb, (const char*)d_gathered, rb, slice, h->b_S,
+                                                         h->b_dslot, h->b_dm, h->b_path, h->hstride, h->d_cnt + 2);
+    CK(cudaGetLastError());
+#else
+    h->d_cnt[2] = 0;
+    for (i64 i = 0; i < nb; ++i) {
+      const i64 k = i / per, j = i - k * per;
+      const char* sl = (const char*)d_gathered + (u64)k * slice;
+      if (j == 0) h->d_cnt[2] = std::max<unsigned int>(h->d_cnt[2], (unsigned int)((const u64*)sl)[0]);
+      const char* row = sl + 16 + (u64)j * rb;
+      h->b_S[i] = *(const i64*)row;
+      h->b_dslot[i] = ((const u32*)row)[2];
+      h->b_dm[i] = ((const u32*)row)[3];
+      memcpy(h->b_path + (u64)i * h->hstride, row + 16, (size_t)h->hstride * 4);
+    }
+#endif
+    group_rounds(h, h->rs.cb0, nb);
+    replay_commit(h);
+    delta_export(h);
+    replay_after_batch(h);
+    shadow_sync(h);  // regions a growth moved are re-taken whole (the replicas regrow identically)
+    *delta_bytes = (int64_t)delta_bytes_of((u64)h->sh.hdr.n_chunks);
+  });
+}
+
+int e2_shard_delta_copy(e2_handle* h, void* d_dst) {
+  return guard(h, [&] {
+    shard_check(h, true);
+    const u64 n = (u64)h->sh.hdr.n_chunks;
+    char* dst = (char*)d_dst;
+    h2d(dst, &h->sh.hdr, sizeof(DeltaHdr), h->stream);
+    if (n) {
+      d2d(dst + kDeltaHdrBytes, h->sh.dl_idx, n * 8, h->stream);
+      d2d(dst + kDeltaHdrBytes + (n * 8 + 63) / 64 * 64, h->sh.dl_pay, n * 64, h->stream);
+    }
+    ssync(h->stream);
+  });
+}
+
+int e2_shard_apply(e2_handle* h, const void* d_delta, int64_t bytes) {
+  return guard(h, [&] {
+    shard_check(h, false);
+    if (bytes < (int64_t)kDeltaHdrBytes) throw Fail(E2_ERR_ARG, "shard: delta too short");
+    DeltaHdr hd;
+    d2h(&hd, d_delta, sizeof(DeltaHdr), h->stream);
+    ssync(h->stream);
+    if (hd.magic != kDeltaMagic) throw Fail(E2_ERR_ARG, "shard: not a delta");
+    const u64 n = (u64)hd.n_chunks;
+    if ((u64)bytes != delta_bytes_of(n)) throw Fail(E2_ERR_ARG, "shard: delta size mismatch");
+    RegionTab t = state_regions(h);
+    if ((int)hd.n_regions != t.n) throw Fail(E2_ERR_ARG, "shard: region count mismatch");
+    for (int r = 0; r < t.n; ++r)
+      if (hd.region_words[r] != t.words[r]) throw Fail(E2_ERR_ARG, "shard: replica capacity diverged");
+    const char* src = (const char*)d_delta;
+    delta_apply(h, t, n, (const u64*)(src + kDeltaHdrBytes),
+                (const uint4*)(src + kDeltaHdrBytes + (n * 8 + 63) / 64 * 64));
+    h->hot = hd.hot;
+    h->dev_hot_valid = false;
+    push_hot(h);
+    h->want_hstride = std::max(h->want_hstride, (int)hd.want_hstride);
+    h->rs.done = hd.done;
+    if (hd.fail_code) {
+      h->rs.fail_code = hd.fail_code;
+      h->rs.fail = hd.msg;
+      h->rs.stopped = true;
+    }
+    ssync(h->stream);
+    replay_after_batch(h);
+  });
+}
+
+int e2_state_digest(e2_handle* h, uint64_t* out, int32_t cap, int32_t* n_out) {
+  return guard(h, [&] {
+    RegionTab t = state_regions(h);
+    if (cap < t.n + 1) throw Fail(E2_ERR_ARG, "digest: output too small");
+    for (int r = 0; r < t.n; ++r) {
+      // the node pool's live part; every other region whole
+      const u64 words = t.live_words[r];
+#if E2_DEVICE_BUILD
+      unsigned long long* d = talloc<unsigned long long>(1);
+      if (words) {
+        k_digest<<<(unsigned)std::min<u64>((words + 255) / 256, (u64)h->n_sm * 8), 256, 0, h->stream>>>(t.cur[r], words, d);
+        CK(cudaGetLastError());
+      }
+      unsigned long long v = 0;
+      d2h(&v, d, 8, h->stream);
+      ssync(h->stream);
+      dfree(d);
+      out[r] = v;
+#else
+      u64 acc = 0;
+      for (u64 i = 0; i < words; ++i) acc += mix64((i << 32) ^ (u64)t.cur[r][i]);
+      out[r] = acc;
+#endif
+    }
+    Hot hot = h->hot;
+    memset(hot.phase_cycles, 0, sizeof(hot.phase_cycles));
+    hot.phase_last = hot.phase_last1 = 0;
+    u64 acc = 0;
+    const u64* w = (const u64*)&hot;
+    for (size_t i = 0; i < sizeof(Hot) / 8; ++i) acc += mix64(((u64)i << 40) ^ w[i]);
+    out[t.n] = acc;
+    *n_out = t.n + 1;
+  });
+}
+
+int e2_shard_end(e2_handle* h, int64_t* n_done) {
+  if (n_done) *n_done = 0;
+  return guard(h, [&] {
+    if (!h->sh.on) throw Fail(E2_ERR_ARG, "no sharded replay in progress");
+    h->sh.on = false;
+    shadow_free(h);
+    replay_end(h, n_done);
+  });
 }
 
 int e2_profile_get(e2_handle* h, e2_profile* out) {

@@ -383,6 +383,13 @@ class GlobalScheduler:
         self._check(self._lib.e2_debug_dump(self._h, float(now), buf, need.value + 1, ctypes.byref(need)))
         return buf.value.decode()
 
+    def state_digest(self) -> np.ndarray:
+        """Non-mutating digest of the replicated state regions (product only)."""
+        out = np.zeros(32, dtype=np.uint64)
+        n = ctypes.c_int32()
+        self._check(self._lib.e2_state_digest(self._h, _ptr(out), 32, ctypes.byref(n)))
+        return out[: n.value].copy()
+
     # -- batched trace driver ---------------------------------------------
     def replay(self, trace, driver, want_costs: bool = True, want_ratios: bool = False):
         """e2_replay over a :class:`workload.Trace`; returns a :class:`ReplayResult`."""
