@@ -286,6 +286,15 @@ int e2_shard_end(e2_handle* h, int64_t* n_done);
  * mutate the state (unlike an export, which brings hit windows current). */
 int e2_state_digest(e2_handle* h, uint64_t* out, int32_t cap, int32_t* n_out);
 
+/* Streamed traces (product only): with `on`, each e2_replay / e2_replay_device
+ * call continues the previous one as if the chunks were one trace — the
+ * driver clock is kept and the note_finished calls of the previous chunk's
+ * last finish_lag requests fall in the next chunk where a single replay
+ * makes them (config 5 is streamed in chunks).  Decisions of
+ * the concatenated chunks equal one replay of the concatenation.  Mirror-LRU
+ * and no-eviction drivers only.  e2_reset starts a new stream. */
+int e2_replay_set_continue(e2_handle* h, int32_t on);
+
 /* Product only: per-kernel device time (ms) and launch counts accumulated
  * since the last reset, for the bench's roofline (kernel ids below). */
 #define E2_K_MATCH 0  /* K1 batched prefix match */

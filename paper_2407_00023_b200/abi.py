@@ -223,6 +223,7 @@ _PRODUCT_SIGS = {
     "e2_shard_apply": (ctypes.c_int, [_h, _vp, _i64]),
     "e2_shard_end": (ctypes.c_int, [_h, P(_i64)]),
     "e2_state_digest": (ctypes.c_int, [_h, _vp, _i32, P(_i32)]),
+    "e2_replay_set_continue": (ctypes.c_int, [_h, _i32]),
 }
 
 #: Every symbol include/e2sched.h declares (checked by the CPU test suite).

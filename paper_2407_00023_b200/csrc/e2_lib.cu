@@ -491,6 +491,7 @@ struct ReplaySession {
   bool stopped = false;
   i64 n = 0, B = 0, next_b0 = 0, cur_b = 0, done = 0;
   i64 cb0 = 0, cnb = 0;  // the current batch
+  i64 carried = 0;       // streamed replay: requests of the previous chunk at the front of the arrays
   SerialArgs a;
   e2_decision* out = nullptr;  // caller's buffers
   e2_cost* costs = nullptr;
@@ -591,6 +592,19 @@ struct e2_handle {
   i64 req_cap = 0;         // d.req_tail capacity
   ReplaySession rs;
   ShardState sh;
+  // streamed replays (e2_replay_set_continue): the next replay continues the
+  // driver state of the previous one; the last finish_lag requests' ids,
+  // arrivals and output lengths are carried so their note_finished calls
+  // land in the next chunk exactly where a single replay would make them
+  bool cont = false;
+  i64 prev_total = 0;   // requests replayed since the last reset
+  i64 carry_n = 0;
+  i64 *carry_ids = nullptr, *carry_out = nullptr;
+  double* carry_arr = nullptr;
+  i64 carry_cap = 0;
+  i64 *cb_ids = nullptr, *cb_out = nullptr;  // combined [carry | chunk] arrays
+  double* cb_arr = nullptr;
+  i64 cb_cap = 0;
   // profiling
   bool prof = false;
   e2_profile acc;
@@ -1681,7 +1695,8 @@ void e2_destroy(e2_handle* h) {
                   d.xp_slot, d.xp_m, d.xp_cm, d.xp_la0, d.xp_flag,
                   h->tok, h->r_off, h->r_len, h->b_S, h->b_L, h->b_cand, h->b_leader, h->b_o, h->b_dslot, h->b_dm,
                   h->b_path, h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api,
-                  h->st_ids, h->st_out, h->st_offs, h->st_arr, h->st_dec, h->st_cost, h->st_rat};
+                  h->st_ids, h->st_out, h->st_offs, h->st_arr, h->st_dec, h->st_cost, h->st_rat,
+                  h->carry_ids, h->carry_out, h->carry_arr, h->cb_ids, h->cb_out, h->cb_arr};
   for (void* p : ptrs) dfree(p);
 #if E2_DEVICE_BUILD
   for (auto& e : h->ev) {
@@ -1733,7 +1748,13 @@ int e2_reset(e2_handle* h) {
     ssync(h->stream);
     h->tok_len = 0;
     h->queue_stats.clear();
+    h->prev_total = 0;
+    h->carry_n = 0;
   });
+}
+
+int e2_replay_set_continue(e2_handle* h, int32_t on) {
+  return guard(h, [&] { h->cont = on != 0; });
 }
 
 int e2_set_stream(e2_handle* h, void* stream) {
@@ -2077,8 +2098,15 @@ void replay_begin(e2_handle* h, const int32_t* tokens, const int64_t* offsets, c
       if (ids[i] == kNoInflight) throw Fail(E2_ERR_ARG, "request id INT64_MIN is reserved");
   }
   const i64 ntok = offn - off0;
+  // streamed continuation: the previous chunk's last finish_lag requests
+  // go in front (their note_finished calls fall in this chunk)
+  const bool cont = h->cont && h->prev_total > 0;
+  if (cont && drv->eviction == E2_EVICT_FIFO_TAIL)
+    throw Fail(E2_ERR_ARG, "streamed replays support the mirror-LRU and no-eviction drivers only");
+  const i64 C = cont ? std::min<i64>(h->carry_n, std::max<i64>(drv->finish_lag, 0)) : 0;
+  S.carried = C;
   reserve_for(h, n, ntok);
-  reserve_requests(h, n);
+  reserve_requests(h, C + n);
   // token arena: append the trace
   const i64 base_tok = h->tok_len;
   const i64 pad = (4 - (base_tok & 3)) & 3;  // 16-byte align the trace start
@@ -2136,25 +2164,53 @@ void replay_begin(e2_handle* h, const int32_t* tokens, const int64_t* offsets, c
   {
     Timed t(h, E2_K_OTHER);
     h->acc.launches[E2_K_OTHER]++;
-    k_arena_index<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(n, tstart, d_offs, h->r_off, h->r_len, 0);
+    k_arena_index<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(n, tstart, d_offs, h->r_off, h->r_len, C);
     CK(cudaGetLastError());
   }
 #else
   for (i64 i = 0; i < n; ++i) {
-    h->r_off[i] = tstart + d_offs[i] - d_offs[0];
-    h->r_len[i] = d_offs[i + 1] - d_offs[i];
+    h->r_off[C + i] = tstart + d_offs[i] - d_offs[0];
+    h->r_len[C + i] = d_offs[i + 1] - d_offs[i];
   }
 #endif
-  // driver state
-  h->hot.drv_now = 0;
-  for (int g = 0; g < G; ++g) h->hot.fifo_head[g] = h->hot.fifo_tail[g] = 0;
+  if (h->cont) {
+    // combined [carry | chunk] ids, arrivals and output lengths
+    const i64 need = C + n;
+    if (need > h->cb_cap) {
+      dfree(h->cb_ids);
+      dfree(h->cb_arr);
+      dfree(h->cb_out);
+      h->cb_cap = need + need / 4;
+      h->cb_ids = talloc<i64>(h->cb_cap);
+      h->cb_arr = talloc<double>(h->cb_cap);
+      h->cb_out = talloc<i64>(h->cb_cap);
+    }
+    if (C) {
+      d2d(h->cb_ids, h->carry_ids, C * 8, h->stream);
+      d2d(h->cb_arr, h->carry_arr, C * 8, h->stream);
+      d2d(h->cb_out, h->carry_out, C * 8, h->stream);
+      dset(h->r_off, 0, C * 8, h->stream);  // carried requests are never replayed again
+      dset(h->r_len, 0, C * 8, h->stream);
+    }
+    d2d(h->cb_ids + C, d_ids, n * 8, h->stream);
+    d2d(h->cb_arr + C, d_arr, n * 8, h->stream);
+    d2d(h->cb_out + C, d_out, n * 8, h->stream);
+    d_ids = h->cb_ids;
+    d_arr = h->cb_arr;
+    d_out = h->cb_out;
+  }
+  // driver state (a streamed continuation keeps the driver clock)
+  if (!cont) {
+    h->hot.drv_now = 0;
+    for (int g = 0; g < G; ++g) h->hot.fifo_head[g] = h->hot.fifo_tail[g] = 0;
+  }
   push_hot(h);
   S.B = drv->batch > 0 ? drv->batch : 16384;
   reserve_batch(h, std::min<i64>(S.B, n));
-  if (n > h->req_cap) {
+  if (C + n > h->req_cap) {
     dfree(h->d.req_tail);
-    h->d.req_tail = talloc<u32>(n);
-    h->req_cap = n;
+    h->d.req_tail = talloc<u32>(C + n);
+    h->req_cap = C + n;
   }
   SerialArgs& a = S.a;
   memset(&a, 0, sizeof(a));
@@ -2170,9 +2226,10 @@ void replay_begin(e2_handle* h, const int32_t* tokens, const int64_t* offsets, c
   a.S = h->b_S;
   a.lead = h->b_leader;
   a.hint = h->b_path;
-  a.dec = S.d_dec;
-  a.costs = S.d_cost;
-  a.ratios = S.d_rat;
+  // the kernels index every per-request array by the combined index C + i
+  a.dec = S.d_dec ? S.d_dec - C : nullptr;
+  a.costs = S.d_cost ? S.d_cost - C * (G + 1) : nullptr;
+  a.ratios = S.d_rat ? S.d_rat - C * G : nullptr;
   a.trunk = drv->trunk_len;
   a.hw = drv->high_water;
   a.lag = drv->finish_lag;
@@ -2180,7 +2237,9 @@ void replay_begin(e2_handle* h, const int32_t* tokens, const int64_t* offsets, c
   // against the tree at its start, so early batches (a cold tree) would
   // leave most requests without K1 path hints.
   S.cur_b = std::min<i64>(S.B, n <= 4 * kFirstBatch ? kShortFirstBatch : kFirstBatch);
-  S.next_b0 = 0;
+  S.next_b0 = C;
+  S.n = C + n;  // batches run over the combined index range [C, C + n)
+  S.done = C;
   S.active = true;
 }
 
@@ -2234,7 +2293,30 @@ void replay_end(e2_handle* h, int64_t* n_done) {
   if (!S.active) throw Fail(E2_ERR_ARG, "no replay in progress");
   S.active = false;
   prof_flush(h);
-  const i64 done = S.done;
+  const i64 C = S.carried;
+  const i64 done = S.done - C;  // requests of this call decided
+  if (h->cont && S.n > 0) {
+    // keep the last finish_lag requests of [carry | chunk] for the next chunk
+    const i64 upto = S.done;  // combined index one past the last decided request
+    const i64 keep = std::min<i64>(upto, std::max<i64>(S.a.lag, 0));
+    if (keep > h->carry_cap) {
+      dfree(h->carry_ids);
+      dfree(h->carry_arr);
+      dfree(h->carry_out);
+      h->carry_cap = keep + 16;
+      h->carry_ids = talloc<i64>(h->carry_cap);
+      h->carry_arr = talloc<double>(h->carry_cap);
+      h->carry_out = talloc<i64>(h->carry_cap);
+    }
+    if (keep) {
+      d2d(h->carry_ids, S.a.ids + (upto - keep), keep * 8, h->stream);
+      d2d(h->carry_arr, S.a.arr + (upto - keep), keep * 8, h->stream);
+      d2d(h->carry_out, S.a.outl + (upto - keep), keep * 8, h->stream);
+      ssync(h->stream);
+    }
+    h->carry_n = keep;
+  }
+  h->prev_total = h->cont ? h->prev_total + std::max<i64>(done, 0) : 0;
   if (!S.device_ptrs && done > 0) {
     const int G = h->G;
     d2h(S.out, S.d_dec, (size_t)done * sizeof(e2_decision), h->stream);
@@ -2482,6 +2564,7 @@ int e2_shard_begin(e2_handle* h, const int32_t* d_tokens, const int64_t* d_offse
   return guard(h, [&] {
     if (world < 1 || rank < 0 || rank >= world) throw Fail(E2_ERR_ARG, "shard: bad rank/world");
     if (n <= 0) throw Fail(E2_ERR_ARG, "shard: empty trace");
+    if (h->cont) throw Fail(E2_ERR_ARG, "shard: streamed continuation is not supported");
     h->sh.on = true;
     h->sh.rank = rank;
     h->sh.world = world;

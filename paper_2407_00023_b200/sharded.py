@@ -103,6 +103,13 @@ class ShardedReplay:
         if self.world == 1:
             recv.copy_(send)
             return recv
+        if send.is_cuda and dist.get_backend() == "gloo":
+            # gloo has no CUDA all-gather (tests sharing one GPU): stage on the host
+            host = send.cpu()
+            parts = [self.torch.empty_like(host) for _ in range(self.world)]
+            dist.all_gather(parts, host)
+            recv.copy_(self.torch.cat(parts))
+            return recv
         parts = [recv[k * nbytes:(k + 1) * nbytes] for k in range(self.world)]
         dist.all_gather(parts, send)
         return recv

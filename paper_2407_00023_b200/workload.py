@@ -108,54 +108,119 @@ class Config:
         return generate(s, self.seed, self.rps, self.arrival_seed, lib)
 
 
-def mix(traces, token_strides) -> Trace:
-    """Interleave several traces by arrival time (config 5's mixed workload).
+def concat(traces) -> Trace:
+    """Concatenate traces (chunks of one stream) into one."""
+    lens = [t.offsets[-1] - t.offsets[0] for t in traces]
+    offs = [traces[0].offsets[:1] * 0]
+    base = 0
+    for t, ln in zip(traces, lens):
+        offs.append(t.offsets[1:] - t.offsets[0] + base)
+        base += ln
+    return Trace(np.concatenate([t.tokens[t.offsets[0]:t.offsets[-1]] for t in traces]), np.concatenate(offs),
+                 np.concatenate([t.ids for t in traces]), np.concatenate([t.arrivals for t in traces]),
+                 np.concatenate([t.output_lens for t in traces]))
 
-    Each component's token ids are shifted by its stride so unrelated
-    archetypes do not alias; ids stay int32 (the reference's TokenId)."""
-    parts = []
-    for t, stride in zip(traces, token_strides):
-        lens = np.diff(t.offsets)
-        toks = t.tokens.astype(np.int64) + stride
-        if toks.size and (toks.max() > np.iinfo(np.int32).max or toks.min() < 0):
-            raise ValueError("token id space exhausted by the mixture")
-        parts.append((t.arrivals, lens, toks.astype(np.int32), t.output_lens))
-    arr = np.concatenate([p[0] for p in parts])
-    order = np.argsort(arr, kind="stable")
-    lens = np.concatenate([p[1] for p in parts])
-    starts = np.concatenate([np.concatenate([[0], np.cumsum(p[1])[:-1]]) + sum(len(q[2]) for q in parts[:i])
-                             for i, p in enumerate(parts)])
-    toks_all = np.concatenate([p[2] for p in parts])
-    outl = np.concatenate([p[3] for p in parts])
-    n = len(arr)
-    new_off = np.zeros(n + 1, dtype=np.int64)
-    new_off[1:] = np.cumsum(lens[order])
-    tokens = np.empty(int(new_off[-1]), dtype=np.int32)
-    for k, i in enumerate(order):
-        tokens[new_off[k]:new_off[k + 1]] = toks_all[starts[i]:starts[i] + lens[i]]
-    return Trace(tokens, new_off, np.arange(1, n + 1, dtype=np.int64), arr[order].copy(), outl[order].copy())
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _splitmix(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = x.astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+FRESH_BASE = 500_000_000  # the generator's fresh-id region (workload.cpp:25-28)
+FRESH_SPAN = 2_147_483_647 - FRESH_BASE
 
 
 class MixConfig(Config):
     """Config 5: toolbench + doc-QA + programming + tree-of-thought + embodied
-    chains, interleaved by arrival time, on 64 instances with a small cache
-    so the eviction term is active on most decisions."""
+    chains on 64 instances with a small cache, so the eviction term is active
+    on most decisions — generated as a STREAM of independent chunks.
+
+    The reference's generator hands out fresh token ids from one counter
+    (workload.cpp:44) and runs out of int32 ids long before 10M requests.
+    Here chunk c (CHUNK requests) is generated by the same archetype
+    generators with seeds derived from (seed, c, component) and then:
+      * shared-prefix ids (system prompts, tool branches, documents, problem
+        trunks: below 5e8) are kept, shifted per component — they recur
+        across chunks like a real corpus;
+      * fresh ids (unique suffixes, thoughts, observations: >= 5e8) are
+        REUSED: remapped by a 64-bit hash of (id, chunk, component) into
+        [5e8, 2^31-1), so id space never runs out;
+      * the components are interleaved by arrival time inside the chunk and
+        the chunk's arrivals are placed in its own time slot, so arrival
+        times increase across chunks; request ids are the stream index + 1.
+    Chunks are independent, so chunk c can be generated directly (random
+    access) and the stream never has to be held in memory: the replay takes
+    it chunk by chunk (e2_replay_set_continue)."""
 
     COMPONENTS = (("toolbench", 0.4, {}), ("doc_qa", 0.1, {}), ("programming", 0.2, {}),
                   ("tree_of_thought", 0.2, {}), ("embodied_agent", 0.1, {}))
+    CHUNK = 65536
+
+    def _counts(self, q: int):
+        fr = np.array([f for _, f, _ in self.COMPONENTS])
+        base = np.floor(q * fr).astype(np.int64)
+        rem = q * fr - base
+        for i in np.argsort(-rem, kind="stable")[: q - int(base.sum())]:
+            base[i] += 1
+        return base
+
+    def chunk(self, c: int, lib=None, q: int = None) -> Trace:
+        """Chunk c of the stream: requests [c*CHUNK, c*CHUNK + q)."""
+        Q = self.CHUNK
+        q = q if q is not None else min(Q, self.n_requests - c * Q)
+        if q <= 0:
+            raise ValueError("chunk index past the end of the stream")
+        parts = []
+        for k, ((arch, frac, over), cnt) in enumerate(zip(self.COMPONENTS, self._counts(q))):
+            if cnt == 0:
+                continue
+            s = default_spec(arch, lib)
+            s.request_count = int(cnt)
+            for a, v in over.items():
+                setattr(s, a, v)
+            t = generate(s, self.seed + 7919 * c + k, self.rps * frac, self.arrival_seed + 7919 * c + k, lib)
+            tok = t.tokens.astype(np.int64)
+            fresh = tok >= FRESH_BASE
+            salt = np.uint64((c * 64 + k + 1) * 0x9E3779B97F4A7C15 & 0xFFFFFFFFFFFFFFFF)
+            h = _splitmix(tok[fresh].astype(np.uint64) ^ salt)
+            tok[fresh] = FRESH_BASE + (h % np.uint64(FRESH_SPAN)).astype(np.int64)
+            tok[~fresh] += k * 20_000_000
+            parts.append((t.arrivals, np.diff(t.offsets), tok.astype(np.int32), t.output_lens))
+        arr = np.concatenate([p[0] for p in parts])
+        lens = np.concatenate([p[1] for p in parts])
+        toks = np.concatenate([p[2] for p in parts])
+        outl = np.concatenate([p[3] for p in parts])
+        starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        order = np.argsort(arr, kind="stable")
+        lens_o = lens[order]
+        off = np.zeros(q + 1, dtype=np.int64)
+        off[1:] = np.cumsum(lens_o)
+        idx = np.repeat(starts[order] - off[:-1], lens_o) + np.arange(off[-1], dtype=np.int64)
+        span = 1000.0 * Q / self.rps  # the chunk's time slot (ms)
+        a = arr[order]
+        rel = a / (a[-1] + 1000.0 / self.rps)  # in [0, 1), increasing
+        arrivals = c * span + span * rel
+        ids = np.arange(c * Q + 1, c * Q + q + 1, dtype=np.int64)
+        return Trace(toks[idx], off, ids, arrivals, outl[order].copy())
+
+    def chunks(self, n_requests=None, lib=None):
+        """The stream's chunks, in order, up to n_requests (default: all)."""
+        n = n_requests if n_requests is not None else self.n_requests
+        Q = self.CHUNK
+        for c in range((n + Q - 1) // Q):
+            yield self.chunk(c, lib, q=min(Q, n - c * Q))
 
     def trace(self, lib=None, n_requests: Optional[int] = None) -> Trace:
         n = n_requests if n_requests is not None else self.n_requests
-        traces, strides = [], []
-        for k, (arch, frac, over) in enumerate(self.COMPONENTS):
-            s = default_spec(arch, lib)
-            s.request_count = max(1, int(round(n * frac)))
-            for a, v in over.items():
-                setattr(s, a, v)
-            traces.append(generate(s, self.seed + k, self.rps * frac, self.arrival_seed + k, lib))
-            strides.append(k * 20_000_000)
-        t = mix(traces, strides)
-        return t.head(min(n, t.n)) if t.n > n else t
+        if n > 8 * self.CHUNK:
+            raise ValueError("config 5 is a stream: use chunks() and a continued replay beyond 8 chunks")
+        return concat(list(self.chunks(n, lib)))
 
 
 def _cs2_sched(cap=200000):

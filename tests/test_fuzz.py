@@ -154,12 +154,12 @@ def _fuzz(lib, ref_lib, cases, base):
 
 
 def test_fuzz_hostsim(hostsim_lib, true_ref_lib):
-    _fuzz(hostsim_lib, true_ref_lib, 150, 20260815)
+    _fuzz(hostsim_lib, true_ref_lib, 1000, 20260815)  # criterion 1 runs 1000 scenarios (acceptance_main.cpp:63-78)
 
 
 @pytest.mark.gpu
 def test_fuzz_b200(b200_lib, true_ref_lib):
-    _fuzz(b200_lib, true_ref_lib, 150, 20260815)
+    _fuzz(b200_lib, true_ref_lib, 1000, 20260815)
 
 
 def _redirect_probe(lib, ref_lib):

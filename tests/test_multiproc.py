@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, ws, port, lib_path, out_dir, cfg_name, n_req, batch):
+def _worker(rank, ws, port, lib_path, out_dir, cfg_name, n_req, batch, device="cpu"):
     import torch
     import torch.distributed as dist
 
@@ -39,7 +39,10 @@ def _worker(rank, ws, port, lib_path, out_dir, cfg_name, n_req, batch):
     trace = cfg.trace(lib=lib, n_requests=n_req)
     drv = DriverConfig(**{**cfg.driver.__dict__, "batch": batch})
     s = GlobalScheduler(cfg.n_gpus, cfg.sched, policy=cfg.policy, lib=lib)
-    dev = torch.device("cpu")
+    dev = torch.device(device)
+    if dev.type == "cuda":
+        torch.cuda.set_device(dev)
+        lib.e2_set_stream(s._h, torch.cuda.current_stream(dev).cuda_stream)
     rep = sharded.ShardedReplay(s, sharded.trace_tensors(trace, dev), drv, dev, rank, ws)
     digests = []
 
@@ -92,3 +95,29 @@ def test_max_over_ranks_single_process():
     from paper_2407_00023_b200.sharded import max_over_ranks
 
     assert max_over_ranks([1.5, 2.0]) == [1.5, 2.0]
+
+
+@pytest.mark.gpu
+def test_sharded_replay_two_ranks_b200():
+    """The device path of the sharded replay (K1 slices, summary pack/unpack,
+    delta diff/apply kernels) with two ranks sharing cuda:0; gloo moves the
+    CUDA tensors (NCCL needs one GPU per rank).  Same checks as on CPU."""
+    import tempfile
+    from pathlib import Path
+
+    from paper_2407_00023_b200 import abi, workload
+    from paper_2407_00023_b200.scheduler import DriverConfig, GlobalScheduler
+
+    lib = abi.product_lib()
+    with tempfile.TemporaryDirectory() as d:
+        tmp = Path(d)
+        n_req, batch = 40000, 4096
+        mp.spawn(_worker, args=(2, _free_port(), abi.PRODUCT_SO, d, "c4", n_req, batch, "cuda:0"), nprocs=2,
+                 join=True)
+        for f in ("nodes", "la", "hits"):
+            assert np.array_equal(np.load(tmp / f"{f}0.npy"), np.load(tmp / f"{f}1.npy")), f
+        cfg = workload.CONFIGS["c4"]
+        trace = cfg.trace(lib=lib, n_requests=n_req)
+        drv = DriverConfig(**{**cfg.driver.__dict__, "batch": batch})
+        ref = GlobalScheduler(cfg.n_gpus, cfg.sched, policy=cfg.policy, lib=lib).replay(trace, drv)
+        assert np.array_equal(np.load(tmp / "dec.npy"), ref.decisions)
