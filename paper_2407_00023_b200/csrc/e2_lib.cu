@@ -189,28 +189,149 @@ __global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
   }
 }
 
-// Persistent: kMatchBlocksPerSM blocks per SM; each warp takes requests from
-// a global counter (fetched one ahead, so the atomic's latency hides behind
-// the current match) until the batch is drained.
+// The staged top image for the next K1 launch (one block): the distinct
+// level-0 slots of the previous batch's path rows that are still children of
+// the root, most used first, each with the head of its edge while the image
+// budget lasts; entries sorted by first token.
+constexpr u32 kTopSet = 1024;  // distinct level-0 slots tracked (more: the rest probe the child table)
+__global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride, i64 nrows, char* img) {
+  __shared__ u32 key[kTopSet];
+  __shared__ u32 cnt[kTopSet];
+  __shared__ u32 cand[kTopSet], ccnt[kTopSet], rank_[kTopSet], hlen[kTopSet];
+  __shared__ u32 ncand;
+  for (u32 i = threadIdx.x; i < kTopSet; i += blockDim.x) {
+    key[i] = kNil;
+    cnt[i] = 0;
+  }
+  if (threadIdx.x == 0) ncand = 0;
+  __syncthreads();
+  for (i64 w = threadIdx.x; w < nrows; w += blockDim.x) {
+    const u32 v = rows[w * (i64)hstride];
+    if (v == kNil || v == kRoot || v >= g_dev.node_cap) continue;
+    u32 h = (u32)(mix64(v) & (kTopSet - 1));
+    for (u32 probe = 0; probe < 64; ++probe, h = (h + 1) & (kTopSet - 1)) {
+      const u32 prev = atomicCAS(&key[h], kNil, v);
+      if (prev == kNil || prev == v) {
+        atomicAdd(&cnt[h], 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < kTopSet; i += blockDim.x) {
+    const u32 v = key[i];
+    if (v == kNil) continue;
+    const NodeRec* r = grec(g_dev, v);
+    if (r->parent != kRoot || r->edge_len == 0) continue;  // split or pruned since: not a root child now
+    const u32 k = atomicAdd(&ncand, 1u);
+    cand[k] = v;
+    ccnt[k] = cnt[i];
+  }
+  __syncthreads();
+  const u32 nc = ncand;
+  // rank by (count desc, slot asc); keep the first kTopMaxEnt
+  for (u32 i = threadIdx.x; i < nc; i += blockDim.x) {
+    u32 rk = 0;
+    for (u32 j = 0; j < nc; ++j) rk += (ccnt[j] > ccnt[i] || (ccnt[j] == ccnt[i] && cand[j] < cand[i])) ? 1u : 0u;
+    rank_[i] = rk;
+    hlen[i] = min_(grec(g_dev, cand[i])->edge_len, kTopHeadMax) & ~3u;  // whole quads
+  }
+  __syncthreads();
+  const u32 ne = min_(nc, kTopMaxEnt);
+  const u32 body = 16 + 32 * kTopMaxEnt;
+  TopEnt* ents = (TopEnt*)(img + 16);
+  for (u32 i = threadIdx.x; i < nc; i += blockDim.x) {
+    if (rank_[i] >= ne) continue;
+    // heads in rank order while the budget lasts
+    u32 before = 0;
+    for (u32 j = 0; j < nc; ++j)
+      if (rank_[j] < rank_[i]) before += hlen[j];
+    u32 hl = hlen[i];
+    if (body + 4 * (before + hl) > kTopBytes) hl = 0;
+    // position in first-token order among the kept entries
+    const NodeRec* r = grec(g_dev, cand[i]);
+    const i32 t = r->first_tok;
+    u32 pos = 0;
+    for (u32 j = 0; j < nc; ++j)
+      if (rank_[j] < ne && grec(g_dev, cand[j])->first_tok < t) ++pos;
+    TopEnt e;
+    e.tok = t;
+    e.slot = cand[i];
+    e.edge_len = r->edge_len;
+    e.head_len = hl;
+    e.head_off = body + 4 * before;
+    e.pad = 0;
+    e.edge_off = r->edge_off;
+    ents[pos] = e;
+    for (u32 k = 0; k < hl; ++k) ((i32*)(img + e.head_off))[k] = g_dev.tok[r->edge_off + k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32 end = body;
+    for (u32 j = 0; j < ne; ++j) end = max_(end, ents[j].head_off + 4 * ents[j].head_len);
+    TopHdr* hd = (TopHdr*)img;
+    hd->n = ne;
+    hd->bytes = (end + 15) & ~15u;
+    hd->pad[0] = hd->pad[1] = 0;
+  }
+}
+
+// Persistent: kMatchBlocksPerSM blocks per SM; each warp takes kTile
+// requests at a time from a global counter (fetched one ahead, so the
+// atomic's latency hides behind the current match) until the batch is
+// drained.  The block first copies the staged top image into shared memory
+// (one TMA bulk copy).  A tile's level-0 lookups are deduplicated: lanes
+// holding the same first token form a __match_any_sync group and only its
+// lowest lane searches the staged table.
 constexpr int kMatchBlocksPerSM = 4;
+constexpr int kTile = 4;
 __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32, kMatchBlocksPerSM)
     k_match(i64 n, i64 base, const i64* off, const i64* len, i64* S, u32* dslot, u32* dm, u32* path, int hstride,
-            unsigned long long* bytes, unsigned int* max_levels, unsigned int* next) {
+            unsigned long long* bytes, unsigned int* max_levels, unsigned int* next, const char* top_img) {
+  __shared__ __align__(128) char top[kTopBytes];
+  __shared__ __align__(8) u64 top_bar;
+  const bool staged = top_img != nullptr;
+  if (staged) {
+    if (threadIdx.x == 0) {
+      const u32 tb = ((const TopHdr*)top_img)->bytes;
+      mbar_init(&top_bar, 1);
+      mbar_expect_tx(&top_bar, tb);
+      bulk_g2s(top, top_img, tb, &top_bar);
+    }
+    __syncthreads();
+    mbar_wait(&top_bar, 0);
+  }
   unsigned long long acc = 0;
   unsigned int w = 0;
-  if (lane0()) w = atomicAdd(next, 1u);
+  if (lane0()) w = atomicAdd(next, (unsigned)kTile);
   w = shfl(w, 0);
   while ((i64)w < n) {
     unsigned int wn = 0;
-    if (lane0()) wn = atomicAdd(next, 1u);
-    const MatchRes m = match_one(g_dev.tok + off[base + w], len[base + w], path + (i64)w * hstride, hstride);
-    if (lane0()) {
-      S[w] = m.S;
-      dslot[w] = m.div_slot;
-      dm[w] = m.div_m;
-      if (m.levels >= hstride) atomicMax(max_levels, (unsigned int)min_<i64>(m.levels, 0x7fffffff));
+    if (lane0()) wn = atomicAdd(next, (unsigned)kTile);
+    int ent = -1;
+    if (staged) {
+      const i64 q = (i64)w + lane();
+      i32 key = (i32)(0x80000000u | (u32)lane());  // distinct negative sentinels (tokens are >= 0)
+      if (lane() < kTile && q < n && len[base + q] > 0) key = g_dev.tok[off[base + q]];
+      const u32 grp = __match_any_sync(0xffffffffu, key);
+      const int lead = ffs32(grp);
+      if (lane() == lead && key >= 0) ent = top_find(top, key);
+      ent = shfl(ent, lead);
     }
-    acc += (unsigned long long)m.bytes;
+    for (int t = 0; t < kTile; ++t) {
+      const i64 q = (i64)w + t;
+      if (q >= n) break;
+      const int e = shfl(ent, t);
+      const MatchRes m = match_one(g_dev.tok + off[base + q], len[base + q], path + q * hstride, hstride,
+                                   staged ? top : nullptr, e);
+      if (lane0()) {
+        S[q] = m.S;
+        dslot[q] = m.div_slot;
+        dm[q] = m.div_m;
+        if (m.levels >= hstride) atomicMax(max_levels, (unsigned int)min_<i64>(m.levels, 0x7fffffff));
+      }
+      acc += (unsigned long long)m.bytes;
+    }
     w = shfl(wn, 0);
   }
   // algorithmic-byte counter: one global atomic per block
@@ -571,6 +692,7 @@ struct e2_handle {
   size_t pin_cap = 0;
   bool no_pipe = false;      // E2_NO_PIPE=1: single-warp replays (dev comparisons)
   bool no_prefetch = false;  // E2_NO_PREFETCH=1: no prefetch warp (dev comparisons)
+  bool no_top = false;       // E2_NO_TOP=1: K1 without the staged top (dev comparisons)
   unsigned int* d_cnt = nullptr;       // [0] active, [1] collisions, [2] deepest K1 path beyond the hint stride
   int hstride = kPathHint;             // K1 path hints per request (grown when paths get deeper)
   int want_hstride = kPathHint;
@@ -590,6 +712,8 @@ struct e2_handle {
   u32 nsets = 0;          // node-cache sets of the serial kernel
   size_t serial_smem = 0;  // its dynamic shared memory
   i64 req_cap = 0;         // d.req_tail capacity
+  char* top_img = nullptr;  // K1's staged top image (device)
+  i64 top_rows = 0;         // valid rows of b_path from the last K1 batch
   ReplaySession rs;
   ShardState sh;
   // streamed replays (e2_replay_set_continue): the next replay continues the
@@ -1040,17 +1164,30 @@ void k1_slice(e2_handle* h, i64 base, i64 lo, i64 cnt) {
   if (cnt <= 0) return;
   [[maybe_unused]] Dev& d = h->d;  // the host emulation's match reads the arena through it
 #if E2_DEVICE_BUILD
-  const i64 blocks = (cnt + kMatchWarpsPerBlock - 1) / kMatchWarpsPerBlock;
+  const i64 blocks = (cnt + kMatchWarpsPerBlock * kTile - 1) / (kMatchWarpsPerBlock * kTile);
   const unsigned grid = (unsigned)std::min<i64>(blocks, (i64)h->n_sm * kMatchBlocksPerSM);
-  h->acc.launches[E2_K_MATCH]++;
   upload_dev(h);
+  if (!h->top_img) h->top_img = (char*)dalloc(kTopBytes);
+  if (!h->no_top) {
+    // the staged top, from the root children the previous batch walked through
+    // (its path rows, still in b_path: rebuilt before this launch overwrites them)
+    Timed tt(h, E2_K_OTHER);
+    h->acc.launches[E2_K_OTHER]++;
+    k_top_build<<<1, 1024, 0, h->stream>>>(h->b_path, h->hstride, std::min<i64>(h->top_rows, h->bcap), h->top_img);
+    CK(cudaGetLastError());
+  }
+  h->acc.launches[E2_K_MATCH]++;
   dset(h->d_cnt + 2, 0, 8, h->stream);  // [2] deepest path, [3] work counter
-  Timed t(h, E2_K_MATCH);  // the kernel alone (roofline denominator)
-  k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(cnt, base + lo, h->r_off, h->r_len, h->b_S + lo,
-                                                           h->b_dslot + lo, h->b_dm + lo,
-                                                           h->b_path + lo * h->hstride, h->hstride, h->d_bytes,
-                                                           h->d_cnt + 2, h->d_cnt + 3);
-  CK(cudaGetLastError());
+  {
+    Timed t(h, E2_K_MATCH);  // the kernel alone (roofline denominator)
+    k_match<<<grid, kMatchWarpsPerBlock * 32, 0, h->stream>>>(cnt, base + lo, h->r_off, h->r_len, h->b_S + lo,
+                                                             h->b_dslot + lo, h->b_dm + lo,
+                                                             h->b_path + lo * h->hstride, h->hstride, h->d_bytes,
+                                                             h->d_cnt + 2, h->d_cnt + 3,
+                                                             h->no_top ? nullptr : h->top_img);
+    CK(cudaGetLastError());
+  }
+  h->top_rows = lo + cnt;
 #else
   h->d_cnt[2] = 0;
   for (i64 w = lo; w < lo + cnt; ++w) {
@@ -1644,6 +1781,8 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
       h->no_pipe = np && np[0] == '1';
       const char* npf = getenv("E2_NO_PREFETCH");
       h->no_prefetch = npf && npf[0] == '1';
+      const char* ntp = getenv("E2_NO_TOP");
+      h->no_top = ntp && ntp[0] == '1';
     }
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream_handle = h->stream;
@@ -1696,7 +1835,7 @@ void e2_destroy(e2_handle* h) {
                   h->tok, h->r_off, h->r_len, h->b_S, h->b_L, h->b_cand, h->b_leader, h->b_o, h->b_dslot, h->b_dm,
                   h->b_path, h->b_state, h->b_A, h->b_B, h->g_tk, h->g_tv, h->d_cnt, h->d_bytes, h->d_api,
                   h->st_ids, h->st_out, h->st_offs, h->st_arr, h->st_dec, h->st_cost, h->st_rat,
-                  h->carry_ids, h->carry_out, h->carry_arr, h->cb_ids, h->cb_out, h->cb_arr};
+                  h->carry_ids, h->carry_out, h->carry_arr, h->cb_ids, h->cb_out, h->cb_arr, h->top_img};
   for (void* p : ptrs) dfree(p);
 #if E2_DEVICE_BUILD
   for (auto& e : h->ev) {

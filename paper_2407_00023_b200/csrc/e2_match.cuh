@@ -115,6 +115,92 @@ E2_D i64 warp_lcp(const i32* a, const i32* b, i64 lim) {
 #endif
 }
 
+#if E2_WARP
+// ---- staged top of the tree (K1, SURVEY north star) -------------------------
+// Per batch, k_top_build writes an image of the root's hottest children
+// (first token, slot, edge, and the first tokens of each edge) to global
+// memory; every K1 block copies it into shared memory with one TMA bulk copy
+// (cp.async.bulk + mbarrier complete_tx).  Level 0 of a walk then costs no
+// child-table probe and compares the head of its edge from shared memory.
+constexpr u32 kTopBytes = 32 * 1024;
+constexpr u32 kTopMaxEnt = 254;
+constexpr u32 kTopHeadMax = 2048;  // tokens staged per root child at most
+struct TopHdr {
+  u32 n;      // entries, sorted by first token
+  u32 bytes;  // image size (multiple of 16)
+  u32 pad[2];
+};
+struct TopEnt {
+  i32 tok;
+  u32 slot;
+  u32 edge_len;
+  u32 head_len;  // tokens staged (edge tokens [0, head_len))
+  u32 head_off;  // byte offset of the staged tokens in the image (16-aligned)
+  u32 pad;
+  i64 edge_off;
+};
+static_assert(sizeof(TopEnt) == 32, "top entries are 32 bytes");
+
+E2_D u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+E2_D void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+E2_D void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// one 1-D TMA bulk copy global -> shared, completing on `bar`
+E2_D void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+E2_D void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TOPW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra TOPW_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Entry of first token t in the staged table (binary search), or -1.
+E2_D int top_find(const char* top, i32 t) {
+  const TopHdr* h = (const TopHdr*)top;
+  const TopEnt* e = (const TopEnt*)(top + 16);
+  int lo = 0, hi = (int)h->n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (e[mid].tok < t) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < (int)h->n && e[lo].tok == t) ? lo : -1;
+}
+
+// First index in [0, lim) where the staged head a (shared memory, 16-byte
+// aligned) and the prompt b differ, or lim.  Warp-wide, 128 tokens a step.
+E2_D i64 smem_lcp(const i32* a, const i32* b, i64 lim) {
+  for (i64 k0 = 0; k0 < lim; k0 += 128) {
+    const i64 t0 = k0 + 4 * lane();
+    u32 mm = 0;
+    if (t0 < lim) {
+      const int4 av = *(const int4*)(a + t0);
+      const i32 bv[4] = {b[t0], t0 + 1 < lim ? b[t0 + 1] : av.y, t0 + 2 < lim ? b[t0 + 2] : av.z,
+                         t0 + 3 < lim ? b[t0 + 3] : av.w};
+      mm = (av.x != bv[0] ? 1u : 0u) | (av.y != bv[1] ? 2u : 0u) | (av.z != bv[2] ? 4u : 0u) |
+           (av.w != bv[3] ? 8u : 0u);
+      mm &= quad_mask(t0, lim) & 0xfu;
+    }
+    const u32 wm = ballot(mm != 0);
+    if (wm) {
+      const int f = ffs32(wm);
+      return k0 + 4 * f + ffs32(shfl(mm, f));
+    }
+  }
+  return lim;
+}
+#endif
+
 struct MatchRes {
   i64 S;         // matched length against the snapshot
   u32 div_slot;  // node where the walk stopped (kRoot if nothing matched)
@@ -124,7 +210,9 @@ struct MatchRes {
 };
 
 // Warp-wide walk with token comparison; records up to nh path slots.
-E2_D MatchRes match_one(const i32* seq, i64 n, u32* path, int nh) {
+// top/ent (K1): the staged table and this prompt's level-0 entry in it (-1:
+// not staged, probe the child table).
+E2_D MatchRes match_one(const i32* seq, i64 n, u32* path, int nh, const char* top = nullptr, int ent = -1) {
   MatchRes r;
   r.S = 0;
   r.div_slot = kRoot;
@@ -132,7 +220,26 @@ E2_D MatchRes match_one(const i32* seq, i64 n, u32* path, int nh) {
   i64 pos = 0, depth = 0;
   u32 cur = kRoot;
   int level = 0;
-  while (pos < n) {
+  bool stop = false;
+#if E2_WARP
+  if (top && ent >= 0 && n > 0) {
+    // level 0 from shared memory: the first token equals by the table key
+    const TopEnt e = ((const TopEnt*)(top + 16))[ent];
+    const i64 len = e.edge_len, lim = min_(len, n);
+    const i64 hl = min_((i64)e.head_len, lim);
+    i64 m = hl >= 1 ? smem_lcp((const i32*)(top + e.head_off), seq, hl) : 1;
+    if (m == max_<i64>(hl, 1) && m < lim) m += warp_lcp(DEV.tok + e.edge_off + m, seq + m, lim - m);
+    depth = 1;
+    if (path && nh > 0 && lane0()) path[0] = e.slot;
+    level = 1;
+    pos = m;
+    cur = e.slot;
+    r.div_slot = e.slot;
+    r.div_m = (u32)m;
+    stop = m < len;  // the match ends inside the root child
+  }
+#endif
+  while (!stop && pos < n) {
     const u32 ch = child_lookup(cur, seq[pos]);
     depth++;
     if (ch == kNil) break;
