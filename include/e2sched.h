@@ -351,6 +351,48 @@ int e2_generate(const e2_workload_spec* spec, uint64_t seed, double rps, uint64_
                 int64_t* n_requests, int64_t* n_tokens, int32_t* tokens, int64_t* offsets,
                 int64_t* ids, double* arrivals, int64_t* output_lens);
 
+/* ---------------------------------------------------------------------------
+ * Corpus / trace files and the corpus study (workload.cpp:329-601; SURVEY 8(f)
+ * row 4).  Host-side input tooling.  Two-phase reads: pass NULL buffers to
+ * get the sizes.  Parse errors return E2_ERR_ARG with the reference's
+ * "<what> line N: ..." message in e2_last_error(NULL).
+ * ------------------------------------------------------------------------- */
+/* write_corpus_file: "id [arrival %.3f] tok... output_len" per line;
+ * arrivals may be NULL (none written) or per-line via has_arrival. */
+int e2_corpus_write(const char* path, const int32_t* tokens, const int64_t* offsets, const int64_t* ids,
+                    const double* arrivals, const int32_t* has_arrival, const int64_t* output_lens, int64_t n);
+/* read_corpus_file. */
+int e2_corpus_read(const char* path, int64_t* n, int64_t* n_tokens, int32_t* tokens, int64_t* offsets,
+                   int64_t* ids, double* arrivals, int32_t* has_arrival, int64_t* output_lens);
+/* read_trace_file: CSV with a header row, rows stably sorted by arrival. */
+int e2_trace_read(const char* path, int64_t* n, double* arrival_s, int64_t* prompt_len, int64_t* output_len);
+/* synthesize_from_trace: toolbench-shaped prompts of the trace's lengths in
+ * arrival order, ids 1..n, arrivals in ms. */
+int e2_synthesize_from_trace(const e2_workload_spec* content, uint64_t seed, const double* arrival_s,
+                             const int64_t* prompt_len, const int64_t* output_len, int64_t n, int64_t* n_tokens,
+                             int32_t* tokens, int64_t* offsets, int64_t* ids, double* arrivals_ms,
+                             int64_t* output_lens);
+typedef struct {
+  int64_t count;
+  double mean, p50, p99, min, max;
+} e2_dist; /* DistStats (workload.hpp:113-120) */
+typedef struct {
+  int64_t requests;
+  int64_t total_prompt_tokens;
+  int64_t total_output_tokens;
+  int64_t total_shared_tokens;
+  double shared_token_fraction;
+  double mean_request_shared_fraction;
+  double mean_prompt_output_ratio;
+  e2_dist prompt_len;
+  e2_dist output_len;
+  int64_t key_portion_count;
+  double mean_key_portion_len;
+  e2_dist requests_per_shared_sequence;
+} e2_study; /* StudyReport (workload.hpp:126-141) */
+/* analyze: the infinite-cache corpus study (workload.cpp:530-601). */
+int e2_analyze(const int32_t* tokens, const int64_t* offsets, const int64_t* output_lens, int64_t n, e2_study* out);
+
 #ifdef __cplusplus
 }
 #endif

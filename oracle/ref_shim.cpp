@@ -623,4 +623,142 @@ int e2_generate(const e2_workload_spec* spec, uint64_t seed, double rps, uint64_
   }
 }
 
+
+// ---- corpus / trace IO and the study (workload.hpp:85-143) -----------------
+int e2_corpus_write(const char* path, const int32_t* tokens, const int64_t* offsets, const int64_t* ids,
+                    const double* arrivals, const int32_t* has_arrival, const int64_t* output_lens, int64_t n) {
+  try {
+    Corpus c(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      c[i].id = ids[i];
+      if (arrivals && (!has_arrival || has_arrival[i])) c[i].arrival_ms = arrivals[i];
+      c[i].prompt.assign(tokens + offsets[i], tokens + offsets[i + 1]);
+      c[i].output_len = output_lens[i];
+    }
+    write_corpus_file(c, path);
+    return E2_OK;
+  } catch (const ParseError& e) {
+    g_create_err = e.what();
+    return E2_ERR_ARG;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return E2_ERR_CONFIG;
+  }
+}
+
+int e2_corpus_read(const char* path, int64_t* n, int64_t* n_tokens, int32_t* tokens, int64_t* offsets, int64_t* ids,
+                   double* arrivals, int32_t* has_arrival, int64_t* output_lens) {
+  try {
+    const Corpus c = read_corpus_file(path);
+    int64_t nt = 0;
+    for (const auto& e : c) nt += static_cast<int64_t>(e.prompt.size());
+    *n = static_cast<int64_t>(c.size());
+    *n_tokens = nt;
+    if (!tokens) return E2_OK;
+    int64_t off = 0;
+    for (size_t i = 0; i < c.size(); ++i) {
+      offsets[i] = off;
+      std::copy(c[i].prompt.begin(), c[i].prompt.end(), tokens + off);
+      off += static_cast<int64_t>(c[i].prompt.size());
+      ids[i] = c[i].id;
+      arrivals[i] = c[i].arrival_ms.value_or(0.0);
+      has_arrival[i] = c[i].arrival_ms ? 1 : 0;
+      output_lens[i] = c[i].output_len;
+    }
+    offsets[c.size()] = off;
+    return E2_OK;
+  } catch (const ParseError& e) {
+    g_create_err = e.what();
+    return E2_ERR_ARG;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return E2_ERR_CONFIG;
+  }
+}
+
+int e2_trace_read(const char* path, int64_t* n, double* arrival_s, int64_t* prompt_len, int64_t* output_len) {
+  try {
+    const std::vector<TraceRow> rows = read_trace_file(path);
+    *n = static_cast<int64_t>(rows.size());
+    if (!arrival_s) return E2_OK;
+    for (size_t i = 0; i < rows.size(); ++i) {
+      arrival_s[i] = rows[i].arrival_s;
+      prompt_len[i] = rows[i].prompt_len;
+      output_len[i] = rows[i].output_len;
+    }
+    return E2_OK;
+  } catch (const ParseError& e) {
+    g_create_err = e.what();
+    return E2_ERR_ARG;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return E2_ERR_CONFIG;
+  }
+}
+
+int e2_synthesize_from_trace(const e2_workload_spec* content, uint64_t seed, const double* arrival_s,
+                             const int64_t* prompt_len, const int64_t* output_len, int64_t n, int64_t* n_tokens,
+                             int32_t* tokens, int64_t* offsets, int64_t* ids, double* arrivals_ms,
+                             int64_t* output_lens) {
+  try {
+    std::vector<TraceRow> rows(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) rows[i] = TraceRow{arrival_s[i], prompt_len[i], output_len[i]};
+    WorkloadSpec s = WorkloadSpec::archetype_default(Archetype::Toolbench);
+    s.system_prompt_len = content->system_prompt_len;
+    s.branch_count = static_cast<int>(content->branch_count);
+    s.branch_len = content->branch_len;
+    s.popularity = content->zipf ? Popularity::Zipf : Popularity::Uniform;
+    s.zipf_s = content->zipf_s;
+    const Corpus c = synthesize_from_trace(rows, s, seed);
+    int64_t nt = 0;
+    for (const auto& e : c) nt += static_cast<int64_t>(e.prompt.size());
+    *n_tokens = nt;
+    if (!tokens) return E2_OK;
+    int64_t off = 0;
+    for (size_t i = 0; i < c.size(); ++i) {
+      offsets[i] = off;
+      std::copy(c[i].prompt.begin(), c[i].prompt.end(), tokens + off);
+      off += static_cast<int64_t>(c[i].prompt.size());
+      ids[i] = c[i].id;
+      arrivals_ms[i] = *c[i].arrival_ms;
+      output_lens[i] = c[i].output_len;
+    }
+    offsets[c.size()] = off;
+    return E2_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return E2_ERR_CONFIG;
+  }
+}
+
+static e2_dist to_dist(const DistStats& d) { return e2_dist{d.count, d.mean, d.p50, d.p99, d.min, d.max}; }
+
+int e2_analyze(const int32_t* tokens, const int64_t* offsets, const int64_t* output_lens, int64_t n, e2_study* out) {
+  try {
+    Corpus c(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      c[i].id = i + 1;
+      c[i].prompt.assign(tokens + offsets[i], tokens + offsets[i + 1]);
+      c[i].output_len = output_lens[i];
+    }
+    const StudyReport r = analyze(c);
+    out->requests = r.requests;
+    out->total_prompt_tokens = r.total_prompt_tokens;
+    out->total_output_tokens = r.total_output_tokens;
+    out->total_shared_tokens = r.total_shared_tokens;
+    out->shared_token_fraction = r.shared_token_fraction;
+    out->mean_request_shared_fraction = r.mean_request_shared_fraction;
+    out->mean_prompt_output_ratio = r.mean_prompt_output_ratio;
+    out->prompt_len = to_dist(r.prompt_len);
+    out->output_len = to_dist(r.output_len);
+    out->key_portion_count = r.key_portion_count;
+    out->mean_key_portion_len = r.mean_key_portion_len;
+    out->requests_per_shared_sequence = to_dist(r.requests_per_shared_sequence);
+    return E2_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return E2_ERR_CONFIG;
+  }
+}
+
 }  // extern "C"

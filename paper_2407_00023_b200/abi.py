@@ -226,6 +226,40 @@ _PRODUCT_SIGS = {
     "e2_replay_set_continue": (ctypes.c_int, [_h, _i32]),
 }
 
+class DistC(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64)] + [(n, ctypes.c_double) for n in ("mean", "p50", "p99", "min", "max")]
+
+
+class StudyC(ctypes.Structure):
+    _fields_ = [
+        ("requests", ctypes.c_int64),
+        ("total_prompt_tokens", ctypes.c_int64),
+        ("total_output_tokens", ctypes.c_int64),
+        ("total_shared_tokens", ctypes.c_int64),
+        ("shared_token_fraction", ctypes.c_double),
+        ("mean_request_shared_fraction", ctypes.c_double),
+        ("mean_prompt_output_ratio", ctypes.c_double),
+        ("prompt_len", DistC),
+        ("output_len", DistC),
+        ("key_portion_count", ctypes.c_int64),
+        ("mean_key_portion_len", ctypes.c_double),
+        ("requests_per_shared_sequence", DistC),
+    ]
+
+
+#: Corpus / trace files and the study (product and reference shim).
+_CORPUS_SIGS = {
+    "e2_corpus_write": (ctypes.c_int, [ctypes.c_char_p, _vp, _vp, _vp, _vp, _vp, _vp, _i64]),
+    "e2_corpus_read": (ctypes.c_int, [ctypes.c_char_p, P(_i64), P(_i64), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "e2_trace_read": (ctypes.c_int, [ctypes.c_char_p, P(_i64), _vp, _vp, _vp]),
+    "e2_synthesize_from_trace": (
+        ctypes.c_int,
+        [P(WorkloadSpecC), _u64, _vp, _vp, _vp, _i64, P(_i64), _vp, _vp, _vp, _vp, _vp],
+    ),
+    "e2_analyze": (ctypes.c_int, [_vp, _vp, _vp, _i64, P(StudyC)]),
+}
+_PRODUCT_SIGS.update(_CORPUS_SIGS)
+
 #: Every symbol include/e2sched.h declares (checked by the CPU test suite).
 DECLARED_SYMBOLS = tuple(_SIGS) + tuple(_PRODUCT_SIGS)
 

@@ -258,3 +258,87 @@ CONFIGS = {
         DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=28500, finish_lag=2000),
     ),
 }
+
+
+# --------------------------------------------------------------------------
+# corpus / trace files and the corpus study (workload.cpp:329-601), C ABI
+# --------------------------------------------------------------------------
+def _lib_err(lib, rc):
+    if rc != abi.E2_OK:
+        msg = lib.e2_last_error(None).decode()
+        raise ValueError(msg) if rc == abi.E2_ERR_ARG else RuntimeError(msg)
+
+
+def write_corpus(path: str, trace: Trace, with_arrivals: bool = True, lib=None) -> None:
+    lib = lib or abi.product_lib()
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    toks = np.ascontiguousarray(trace.tokens, dtype=np.int32)
+    rc = lib.e2_corpus_write(path.encode(), p(toks), p(trace.offsets), p(trace.ids),
+                             p(trace.arrivals) if with_arrivals else None, None, p(trace.output_lens), trace.n)
+    _lib_err(lib, rc)
+
+
+def read_corpus(path: str, lib=None):
+    """(Trace, has_arrival) of a corpus file; arrivals are 0 where absent."""
+    lib = lib or abi.product_lib()
+    n, nt = ctypes.c_int64(), ctypes.c_int64()
+    _lib_err(lib, lib.e2_corpus_read(path.encode(), ctypes.byref(n), ctypes.byref(nt), None, None, None, None, None,
+                                     None))
+    toks = np.zeros(nt.value + 64, dtype=np.int32)
+    off = np.zeros(n.value + 1, dtype=np.int64)
+    ids = np.zeros(n.value, dtype=np.int64)
+    arr = np.zeros(n.value, dtype=np.float64)
+    has = np.zeros(n.value, dtype=np.int32)
+    outl = np.zeros(n.value, dtype=np.int64)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _lib_err(lib, lib.e2_corpus_read(path.encode(), ctypes.byref(n), ctypes.byref(nt), p(toks), p(off), p(ids), p(arr),
+                                     p(has), p(outl)))
+    return Trace(toks[: nt.value], off, ids, arr, outl), has
+
+
+def read_trace(path: str, lib=None):
+    """(arrival_s, prompt_len, output_len) of a request-trace CSV, by arrival."""
+    lib = lib or abi.product_lib()
+    n = ctypes.c_int64()
+    _lib_err(lib, lib.e2_trace_read(path.encode(), ctypes.byref(n), None, None, None))
+    a = np.zeros(n.value, dtype=np.float64)
+    pl = np.zeros(n.value, dtype=np.int64)
+    ol = np.zeros(n.value, dtype=np.int64)
+    p = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+    _lib_err(lib, lib.e2_trace_read(path.encode(), ctypes.byref(n), p(a), p(pl), p(ol)))
+    return a, pl, ol
+
+
+def synthesize_from_trace(arrival_s, prompt_len, output_len, content: abi.WorkloadSpecC, seed: int, lib=None) -> Trace:
+    lib = lib or abi.product_lib()
+    a = np.ascontiguousarray(arrival_s, dtype=np.float64)
+    pl = np.ascontiguousarray(prompt_len, dtype=np.int64)
+    ol = np.ascontiguousarray(output_len, dtype=np.int64)
+    n = len(a)
+    p = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+    nt = ctypes.c_int64()
+    args = [ctypes.byref(content), seed, p(a), p(pl), p(ol), n, ctypes.byref(nt)]
+    _lib_err(lib, lib.e2_synthesize_from_trace(*args, None, None, None, None, None))
+    toks = np.zeros(nt.value + 64, dtype=np.int32)
+    off = np.zeros(n + 1, dtype=np.int64)
+    ids = np.zeros(n, dtype=np.int64)
+    arr = np.zeros(n, dtype=np.float64)
+    outl = np.zeros(n, dtype=np.int64)
+    _lib_err(lib, lib.e2_synthesize_from_trace(*args, p(toks), p(off), p(ids), p(arr), p(outl)))
+    return Trace(toks[: nt.value], off, ids, arr, outl)
+
+
+def analyze(trace: Trace, lib=None) -> dict:
+    """The corpus study (StudyReport, workload.hpp:126-141) as a dict."""
+    lib = lib or abi.product_lib()
+    st = abi.StudyC()
+    p = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+    toks = np.ascontiguousarray(trace.tokens, dtype=np.int32)
+    _lib_err(lib, lib.e2_analyze(p(toks), p(trace.offsets), p(trace.output_lens), trace.n, ctypes.byref(st)))
+
+    def conv(x):
+        if isinstance(x, abi.DistC):
+            return {f: getattr(x, f) for f, _ in abi.DistC._fields_}
+        return x
+
+    return {f: conv(getattr(st, f)) for f, _ in abi.StudyC._fields_}

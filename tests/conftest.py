@@ -38,14 +38,14 @@ def _stale(target, deps):
 
 
 def build_hostsim() -> str:
-    srcs = [os.path.join(CSRC, "e2_lib.cu"), os.path.join(CSRC, "workload_gen.cpp")]
+    srcs = [os.path.join(CSRC, "e2_lib.cu"), os.path.join(CSRC, "workload_gen.cpp"), os.path.join(CSRC, "corpus.cpp")]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(REPO, "include", "e2sched.h")]
     if _stale(HOSTSIM_SO, deps):
         os.makedirs(BUILD, exist_ok=True)
         tmp = HOSTSIM_SO + f".{os.getpid()}.tmp"
         cmd = [
             "/usr/bin/g++", "-x", "c++", "-std=c++17", "-O2", "-DE2_HOSTSIM", "-ffp-contract=off", "-fPIC", "-shared",
-            "-I" + os.path.join(REPO, "include"), "-I" + CSRC, "-o", tmp, srcs[0], "-x", "c++", srcs[1],
+            "-I" + os.path.join(REPO, "include"), "-I" + CSRC, "-o", tmp, srcs[0], "-x", "c++", srcs[1], srcs[2],
         ]
         subprocess.run(cmd, check=True)
         os.replace(tmp, HOSTSIM_SO)
