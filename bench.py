@@ -317,7 +317,10 @@ class DeviceReplay:
         self.t_out = torch.from_numpy(trace.output_lens).to(dev)
         self.o_dec = torch.empty(self.n * DECISION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         self.o_cost = torch.empty(self.n * (self.G + 1) * COST_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        self.stream = torch.cuda.current_stream(dev)
+        # a dedicated stream: the library's launches and the timing events
+        # share it (the legacy default stream would leave the library on its
+        # own non-blocking stream)
+        self.stream = torch.cuda.Stream(dev)
         self.sched = GlobalScheduler(self.G, cfg.sched, policy=cfg.policy, lib=self.lib)
         self.h = self.sched._h
         self.lib.e2_set_stream(self.h, ctypes.c_void_p(self.stream.cuda_stream))

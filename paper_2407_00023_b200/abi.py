@@ -258,6 +258,9 @@ _CORPUS_SIGS = {
     ),
     "e2_analyze": (ctypes.c_int, [_vp, _vp, _vp, _i64, P(StudyC)]),
 }
+#: Entry points only the product (and its host emulation) exports: the
+#: checkers have no sharded or streamed replay.
+PRODUCT_ONLY = tuple(_PRODUCT_SIGS)
 _PRODUCT_SIGS.update(_CORPUS_SIGS)
 
 #: Every symbol include/e2sched.h declares (checked by the CPU test suite).

@@ -24,6 +24,7 @@ struct Scr {
   i32 n_costs;
   i32 loads_ok;  // loads[] hold load_ms at this request's `now` (update_redirects ran)
   i32 spec_bad;  // a speculative decide gave up (see decide)
+  i32 spec_walked;  // ... after a complete walk that probed no table (reusable if the path is untouched)
   i32 fix_D;     // path levels whose LRU fixes path_update_par deferred (0: none)
   i32 cpath;     // levels of the committed path in pslot (-1: not recorded)
   i32 win_done;  // the scheduled-window entry was appended before the commit (pipelined replay)
@@ -151,9 +152,73 @@ E2_HD bool win_add_comp(int g, double now, i64 out) {
 // prefix nodes above some logged slots (they copied the stamp), found as
 // the parent chain between consecutive logged slots.  Unlogged entries walk
 // the parent chain from their tail slot.  Warp-wide.
+E2_DNI void hits_catchup_one(int g);
+
 E2_DNI void hits_catchup(int g) {
   const int G = DEV.cfg.G;
+#if E2_WARP
+  // Several expired entries per warp step: consecutive entries' logged paths
+  // are contiguous in the path-log ring, so lane l takes ring position
+  // pl_head + l and the group undoes up to kWidth levels in one pass (the
+  // decrements are atomic: the group's paths share their upper nodes).
+  constexpr int kGroup = 8;
   while (HOT.ws_done[g] < HOT.ws_head[g]) {
+    const u64 d0 = HOT.ws_done[g];
+    const int avail = (int)min_<u64>(HOT.ws_head[g] - d0, (u64)kGroup);
+    u32 plen = kNil;
+    if (lane() < avail) plen = DEV.win[wslot(g, d0 + (u64)lane())].plen;
+    // take entries while they are logged and their levels fit the warp
+    u32 take = 0, total = 0;
+    for (int j = 0; j < avail; ++j) {
+      const u32 pj = shfl(plen, j);
+      if (pj == kNil || total + pj > (u32)kWidth) break;
+      total += pj;
+      take++;
+    }
+    if (take == 0) {
+      // an unlogged entry, or one path longer than a warp: one entry, as below
+      hits_catchup_one(g);
+      continue;
+    }
+    // lane l: its entry's first level?  (exclusive prefix sums of plen)
+    bool first = false;
+    {
+      u32 acc = 0;
+      for (u32 j = 0; j < take; ++j) {
+        if ((u32)lane() == acc) first = true;
+        acc += shfl(plen, (int)j);
+      }
+    }
+    const u64 h0 = HOT.pl_head[g], pmask = DEV.pcap - 1;
+    const u32* ring = DEV.plog + (u64)g * DEV.pcap;
+    if ((u32)lane() < total) {
+      const u32 v = ring[(h0 + (u64)lane()) & pmask];
+      const u32 up = first ? kRoot : ring[(h0 + (u64)lane() - 1) & pmask];
+      NodeRec* r = npoke(v);
+      atomicAdd(&rhits(r, G)[g], -1);
+      // prefix halves a split inserted above v since the commit
+      for (u32 p = r->parent; p != up && p != kRoot && p != kNil;) {
+        NodeRec* rp = npoke(p);
+        atomicAdd(&rhits(rp, G)[g], -1);
+        p = rp->parent;
+      }
+    }
+    wsync();
+    if (lane0()) {
+      HOT.pl_head[g] = h0 + total;
+      HOT.ws_done[g] = d0 + take;
+    }
+    wsync();
+  }
+#else
+  while (HOT.ws_done[g] < HOT.ws_head[g]) hits_catchup_one(g);
+#endif
+}
+
+// One expired window entry of instance g: undo its hit stamps.
+E2_DNI void hits_catchup_one(int g) {
+  const int G = DEV.cfg.G;
+  {
     const WinEnt e = DEV.win[wslot(g, HOT.ws_done[g])];
     if (e.plen != kNil) {
       const u64 h0 = HOT.pl_head[g], pmask = DEV.pcap - 1;
@@ -411,6 +476,7 @@ E2_DNI Walk walk_known(const i32* seq, i64 L, const u32* hint, int nhint, i64* e
       }
     }
     if (ch == kNil) {
+      note_probe();
       ch = child_lookup(cur, t);
       if (ch == kNil) {
         w.ok = false;
@@ -539,6 +605,7 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
         w.last_m = lm;
         if (lastm) done = true;  // reached L (or the match ends inside this edge)
         if (lm < ll) done = true;
+        PHASE_MARK(38);  // walk: hinted levels
         continue;
       }
       // The next hint does not hang off `cur`.  Splits since K1 keep every
@@ -558,18 +625,24 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
           // after `pos` continue this prompt's path (both share [0, L))
           hint = hint2;
           hS = L;
-          int idx = min_(np, nhint - 1);
-          while (idx > 0) {
-            const u32 c2 = hint[idx - 1];
-            if (c2 == kNil || npeek(c2)->depth >= pos) --idx;
-            else break;
+          // the leader's path is top-down with strictly increasing depths:
+          // resume at its first entry starting at or after `pos` (the count
+          // of entries starting below it), kWidth entries per step
+          int idx = 0;
+          for (int b0 = 0; b0 < nhint - 1; b0 += kWidth) {
+            const int j = b0 + lane();
+            bool below = false;
+            if (j < nhint - 1) {
+              const u32 c2 = hint[j];
+              below = c2 != kNil && (i64)npeek(c2)->depth < pos;
+            }
+            const u32 bm = ballot(below);
+            const int run = (bm == kFull) ? kWidth : ffs32(~bm);
+            idx = b0 + run;
+            if (run < kWidth) break;
           }
-          while (idx < nhint - 1) {
-            const u32 c2 = hint[idx];
-            if (c2 != kNil && npeek(c2)->depth < pos) ++idx;
-            else break;
-          }
-          hi = idx;
+          hi = min_(idx, nhint - 1);
+          PHASE_MARK(39);  // walk: switch to the leader's committed path
           continue;
         }
         fast = false;
@@ -634,11 +707,13 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
         if (lm < ll) done = true;
         if (usedc < chunk) break;  // a chain node starts past hS: re-evaluated next pass
       }
+      PHASE_MARK(40);  // walk: climb across splits
       continue;
     }
     // no usable hint: one child-table probe per level
     const i32 t = seq[pos];
     PHASE_COUNT(12);
+    note_probe();
     const u32 ch = child_lookup(cur, t);
     if (ch == kNil) {
       w.ok = false;
@@ -661,6 +736,7 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
     w.last_m = m;
     if (m < len) break;
   }
+  PHASE_MARK(41);  // walk: child-table probes
   if (lane0()) s->npath = np;
   wsync();
   if (!w.ok) return w;
@@ -978,8 +1054,12 @@ E2_D bool any_need(const Scr* s, u64 set, i64 n) {
 // eviction term, the cost of instance g depends on the eviction only through
 // need = missed - (cap - cached_tokens[g]) <= 0, which an eviction (cached
 // tokens only decrease) cannot turn positive.
+// reuse_walk: the walk of a speculative decide of this request that gave up
+// later (an eviction term was due) and whose path the concurrent eviction
+// did not touch: w and s's path/extents are current, the walk is skipped.
 E2_D Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint, i64 hS, double now, Walk& w,
-                  bool spec = false, const i64* lead = nullptr, const u32* hint_rows = nullptr) {
+                  bool spec = false, const i64* lead = nullptr, const u32* hint_rows = nullptr,
+                  bool reuse_walk = false) {
   Dec r;
   r.branch = 1;
   r.gpu = -1;
@@ -995,10 +1075,12 @@ E2_D Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint
   if (lane0()) {
     s->n_costs = 0;
     s->spec_bad = 0;
+    if (!reuse_walk) s->spec_walked = 0;
   }
   wsync();
 #define SPEC_FAIL()           \
   do {                        \
+    PHASE_COUNT(42);          \
     if (lane0()) s->spec_bad = 1; \
     wsync();                  \
     r.ok = 0;                 \
@@ -1022,12 +1104,23 @@ E2_D Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint
   if (!spec && lane0()) HOT.stats[kStTreeReads]++;  // a validated speculative decide is counted by the caller
   wsync();
   PHASE_MARK(32);
-  w = walk_par(seq, L, hint, nhint, s, hS, lead, hint_rows);
-  if (!w.ok && s->npath < 0) {
-    if (spec) SPEC_FAIL();
-    w = walk_known(seq, L, hint, nhint, s->ext);
+  if (!reuse_walk) {
+#if E2_WARP
+    if (lane0()) g_probed = 0;
+    wsync();
+#endif
+    w = walk_par(seq, L, hint, nhint, s, hS, lead, hint_rows);
+    if (!w.ok && s->npath < 0) {
+      if (spec) SPEC_FAIL();
+      w = walk_known(seq, L, hint, nhint, s->ext);
+    }
+    PHASE_MARK(6);
+#if E2_WARP
+    if (spec && g_probed) SPEC_FAIL();  // the table may lack the previous leaf's entry yet
+#endif
+    if (spec && w.ok && lane0()) s->spec_walked = 1;
+    wsync();
   }
-  PHASE_MARK(6);
   if (!w.ok) {
     if (spec) SPEC_FAIL();
     if (lane0()) set_err(kErrSim, kWhyWalk);
@@ -1123,9 +1216,12 @@ E2_D Dec decide(Scr* s, const i32* seq, i64 n, i64 L, const u32* hint, int nhint
       r.branch = 1;
       const u64 all = G == 64 ? ~0ull : ((1ull << G) - 1);
       if (spec && any_need(s, all, n)) SPEC_FAIL();
+      PHASE_MARK(46);  // explore: ratios
       cost_prepare_set(s, all, n, now);
+      PHASE_MARK(44);  // explore: window prune + hit catch-up
       for (int g = lane(); g < G; g += kWidth) put_cost(s, g, g, cost_for(g, n - s->ext[g], now, s));
       wsync();
+      PHASE_MARK(45);  // explore: every instance's cost
       if (lane0()) s->n_costs = G;
       wsync();
       r.gpu = pick_min(s, G);

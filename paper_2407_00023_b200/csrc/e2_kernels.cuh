@@ -520,7 +520,22 @@ E2_D void wait_pause() {
   if (E2_WAIT_NS > 0) __nanosleep(E2_WAIT_NS);
 }
 
-E2_D void bar_pair(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+// bar.sync is the .aligned barrier: the whole warp must arrive converged,
+// and the flag polls before it let lanes leave their loops on different
+// iterations (compute-sanitizer synccheck), so reconverge first.
+E2_D void bar_pair(int id) {
+  __syncwarp();
+  asm volatile("barrier.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+// Flag hand-offs between the pipeline's warps (shared memory): the writer
+// stores its data, fences (__threadfence_block) and then raises a volatile
+// flag; the reader polls the flag and fences again before reading the data
+// (acquire), then reconverges.
+E2_D void acquire_after_poll() {
+  __threadfence_block();
+  wsync();
+}
 
 // Warp 0, after barrier 1: did the eviction that ran beside a speculative
 // decide touch any node of the decided path?
@@ -646,6 +661,7 @@ E2_D void prefetch_loop(const SerialArgs& a) {
 E2_D void books_loop(Scr* s2, const SerialArgs& a, Pipe* pp) {
   for (i64 ci = 0;; ++ci) {
     while (pp->ready != ci + 1 && !*(volatile i32*)&pp->stop) wait_pause();
+    acquire_after_poll();
     if (pp->ready != ci + 1) break;
     if (pp->c_defer) inflight_insert(pp->c_id, pp->c_g, pp->c_cached, pp->c_n, pp->c_arr, pp->c_root);
     replay_finish(a, ci, pp->c_now);
@@ -691,14 +707,27 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       // the LRU re-indexing of the path warp 0 is committing, beside the
       // rest of its commit (it must precede this warp's evictions)
       while (pp->fix_ready != ci + 1 && !*(volatile i32*)&pp->stop) wait_pause();
+      acquire_after_poll();
       PHASE_MARK1(31);  // waiting for warp 0's path update
       if (pp->fix_ready == ci + 1 && pp->fs->fix_D > 0) path_lru_fix(pp->fs, pp->fs->fix_D, pp->fg);
       PHASE_MARK1(20);  // LRU fixes
       bar_pair(2);
       PHASE_MARK1(23);
-      if (pp->stop) break;
+      if (pp->stop) {
+        if (g_ctd.pending) {  // the failing request's leaf: keep the table consistent
+          child_insert(g_ctd.parent, g_ctd.tok, g_ctd.child);
+          if (lane0()) g_ctd.pending = 0;
+          wsync();
+        }
+        break;
+      }
       if (lane0()) g_ntouch = 0;
       wsync();
+      if (g_ctd.pending) {  // warp 0's deferred child-table insert of request pp->li's leaf
+        child_insert(g_ctd.parent, g_ctd.tok, g_ctd.child);
+        if (lane0()) g_ctd.pending = 0;
+        wsync();
+      }
       const Scr* sb = pp->s;
       pli = pp->li;
       pdec = pp->dec;
@@ -719,6 +748,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     // this request's `now` and loads)
     if (i > 0) {
       while (pp->books_done < i) wait_pause();
+      acquire_after_poll();
       PHASE(30);  // waiting for warp 3's bookkeeping
     }
     const double now = pre_done ? s->pre_now : replay_pre(s, a, i);
@@ -740,16 +770,19 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       break;
     }
     bool ok;
-    bool valid = specd && !s->spec_bad && !spec_conflict(s);
+    const bool walked = specd && s->spec_walked;
+    const bool conflict = walked && spec_conflict(s);
+    if (conflict) PHASE_COUNT(43);  // the eviction touched the decided path
+    bool valid = specd && !s->spec_bad && !conflict;
     if (valid) {
       if (DEV.cfg.mode == 0 && lane0()) HOT.stats[kStTreeReads]++;
       wsync();
       PHASE(34);  // validation
     } else {
-      PHASE_COUNT(17);  // speculation redone
+      PHASE_COUNT(17);  // speculation redone (keeping its walk when the path is untouched)
       const i64 r = a.base + i;
       dec = decide(s, DEV.tok + a.off[r], a.len[r], a.L[i], a.hint + i * a.hstride, a.hstride, a.S[i], now, w, false,
-                   a.lead ? a.lead + i : nullptr, a.hint);
+                   a.lead ? a.lead + i : nullptr, a.hint, walked && !conflict);
     }
     // hand the inflight record (prefix root known before the insert: the
     // first matched level keeps its id through a split at L; with nothing

@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
     ((u32*)dyn)[2 * ne + i] = 0;
   }
   if (threadIdx.x == 0) {
+    g_ctd.pending = 0;
+    g_defer_ct = (a.kind == 0 && blockDim.x >= 64) ? 1u : 0u;  // the pipelined replay only
+    g_probed = 0;
     g_pf_cur = -1;
     g_pf_stop = 0;
     pipe.ready = 0;
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
   }
   __syncthreads();
   serial_body(ss, a, blockDim.x >= 64 ? &pipe : nullptr);
+  __syncwarp();  // the warps leave their polling loops lane by lane
   __syncthreads();
   if (threadIdx.x < 32) {
     const u64* src = (const u64*)&g_hot;
@@ -247,7 +251,8 @@ __global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride
     for (u32 j = 0; j < nc; ++j)
       if (rank_[j] < rank_[i]) before += hlen[j];
     u32 hl = hlen[i];
-    if (body + 4 * (before + hl) > kTopBytes) hl = 0;
+    if (body + 4 * (before + hl) > kTopBytes) hl = 0;  // over the budget: lookup only
+    const u32 hoff = hl ? body + 4 * before : body;
     // position in first-token order among the kept entries
     const NodeRec* r = grec(g_dev, cand[i]);
     const i32 t = r->first_tok;
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride
     e.slot = cand[i];
     e.edge_len = r->edge_len;
     e.head_len = hl;
-    e.head_off = body + 4 * before;
+    e.head_off = hoff;
     e.pad = 0;
     e.edge_off = r->edge_off;
     ents[pos] = e;
@@ -271,7 +276,7 @@ __global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride
     for (u32 j = 0; j < ne; ++j) end = max_(end, ents[j].head_off + 4 * ents[j].head_len);
     TopHdr* hd = (TopHdr*)img;
     hd->n = ne;
-    hd->bytes = (end + 15) & ~15u;
+    hd->bytes = min_((end + 15) & ~15u, kTopBytes);
     hd->pad[0] = hd->pad[1] = 0;
   }
 }
@@ -284,7 +289,10 @@ __global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride
 // holding the same first token form a __match_any_sync group and only its
 // lowest lane searches the staged table.
 constexpr int kMatchBlocksPerSM = 4;
-constexpr int kTile = 4;
+#ifndef E2_K1_TILE
+#define E2_K1_TILE 2
+#endif
+constexpr int kTile = E2_K1_TILE;  // requests per warp work unit (level-0 lookups deduplicated across them)
 __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32, kMatchBlocksPerSM)
     k_match(i64 n, i64 base, const i64* off, const i64* len, i64* S, u32* dslot, u32* dm, u32* path, int hstride,
             unsigned long long* bytes, unsigned int* max_levels, unsigned int* next, const char* top_img) {
@@ -2912,7 +2920,7 @@ int e2_profile_reset(e2_handle* h, int32_t enable_timing) {
 extern "C" int e2_debug_phases(e2_handle* h, uint64_t* out) {
   return guard(h, [&] {
     pull_hot(h);
-    for (int i = 0; i < 40; ++i) out[i] = h->hot.phase_cycles[i];
+    for (int i = 0; i < 48; ++i) out[i] = h->hot.phase_cycles[i];
   });
 }
 #endif

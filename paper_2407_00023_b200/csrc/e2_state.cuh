@@ -37,8 +37,14 @@ struct NodeRec {
   u64 cmask;      // bit g: cached on instance g
   u64 lamask;     // bit g: last_access[g] entry exists
   i32 nchild;
-  u32 ctpos;  // position of this node's own child-table entry (its parent's key for it)
-  u64 pad1;
+  u32 ctpos;  // position of this node's own child-table entry (its parent's key for it), or kCtInline
+  // One child is kept inline (first token, slot; in_slot 0 = none, the root
+  // is never a child): a lookup reads the parent's header first and probes
+  // the hashed table only for its other children.  Splits link the suffix
+  // here and new leaves land here whenever the parent has none, so chains,
+  // fresh split prefixes and single-child nodes never touch the table.
+  i32 in_tok;
+  u32 in_slot;
   // followed by: double la[G]; i32 hits[G]; i32 ccc[G];
 };
 static_assert(sizeof(NodeRec) == 64, "node header must stay 64 bytes");
@@ -91,6 +97,7 @@ struct CompEnt {
   i64 out;
 };
 
+constexpr u32 kCtInline = 0xfffffffeu;  // ctpos: the node is its parent's inline child
 constexpr u64 kEmptyKey = ~0ull;
 constexpr u64 kTombKey = ~0ull - 1;
 constexpr i64 kNoInflight = INT64_MIN;
@@ -176,7 +183,7 @@ struct Hot {
   i32 err, why;
   i64 err_req;  // request index / op index that failed
   i64 done;     // ops fully processed in the last launch
-  u64 phase_cycles[40];  // E2_PHASES builds: clock64 per replay phase
+  u64 phase_cycles[48];  // E2_PHASES builds: clock64 per replay phase
   u64 phase_last, phase_last1;
 };
 static_assert(sizeof(Hot) % 8 == 0, "Hot is copied as u64 words");

@@ -71,6 +71,28 @@ E2_D void touch(u32 v) {
 E2_HD void touch(u32) {}
 #endif
 
+// Deferred child-table inserts (pipelined replay): a new leaf whose parent
+// already has its inline child needs a hashed-table entry, i.e. one random
+// HBM round trip.  Warp 0 leaves that insert to the eviction warp, which
+// performs it first thing after barrier 2, while warp 0 moves on to the next
+// speculative decide; a speculative walk that probes the table meanwhile
+// gives up (g_probed) and is redone after barrier 1.
+#if E2_WARP
+struct CtDefer {
+  u32 parent, child;
+  i32 tok;
+  u32 pending;
+};
+__shared__ CtDefer g_ctd;
+__shared__ u32 g_defer_ct;  // warp 0 of the pipelined replay defers
+__shared__ u32 g_probed;    // a walk probed the child table
+E2_D void note_probe() {
+  if (lane0()) g_probed = 1;
+}
+#else
+E2_HD void note_probe() {}
+#endif
+
 // E2_PHASES (dev-only instrumented builds): cycles since the previous mark
 // are added to phase_cycles[i].  Compiled out of the product.
 #if defined(E2_PHASES) && E2_DEVICE_BUILD
@@ -315,8 +337,12 @@ E2_DNI Probe ct_probe(u64 key) {
   return Probe{first_free, 0, false};
 }
 
-// warp-wide
+// warp-wide: the inline child first, the table only for the other children
 E2_D u32 child_lookup(u32 parent, i32 tok) {
+  const NodeRec* r = npeek(parent);
+  const u32 is = r->in_slot;
+  if (is != 0 && r->in_tok == tok) return is;
+  if (r->nchild <= (is != 0 ? 1 : 0)) return kNil;  // no child in the table
   Probe p = ct_probe(ckey(parent, tok));
   return p.found ? p.val : kNil;
 }
@@ -324,6 +350,17 @@ E2_D u32 child_lookup(u32 parent, i32 tok) {
 // warp-wide; key must be absent.  Records the entry's position in the
 // child's record (ctpos), so re-pointing or erasing it needs no probe.
 E2_DNI bool child_insert(u32 parent, i32 tok, u32 child) {
+  NodeRec* rp = nget(parent);
+  if (rp->in_slot == 0) {  // the parent's inline child
+    wsync();
+    if (lane0()) {
+      rp->in_tok = tok;
+      rp->in_slot = child;
+      nget_lane(child)->ctpos = kCtInline;
+    }
+    wsync();
+    return true;
+  }
   const u64 key = ckey(parent, tok);
   Probe p = ct_probe(key);
   if (p.found || p.pos == ~0ull) {
@@ -347,6 +384,13 @@ E2_DNI bool child_insert(u32 parent, i32 tok, u32 child) {
 
 // warp-wide; key must be present.
 E2_DNI void child_update(u32 parent, i32 tok, u32 child) {
+  NodeRec* rp = nget(parent);
+  if (rp->in_slot != 0 && rp->in_tok == tok) {
+    wsync();
+    if (lane0()) rp->in_slot = child;
+    wsync();
+    return;
+  }
   Probe p = ct_probe(ckey(parent, tok));
   wsync();
   if (lane0()) {
@@ -360,6 +404,16 @@ E2_DNI void child_update(u32 parent, i32 tok, u32 child) {
 
 // warp-wide
 E2_DNI void child_erase(u32 parent, i32 tok) {
+  NodeRec* rp = nget(parent);
+  if (rp->in_slot != 0 && rp->in_tok == tok) {
+    wsync();
+    if (lane0()) {
+      rp->in_slot = 0;
+      rp->in_tok = 0;
+    }
+    wsync();
+    return;
+  }
   Probe p = ct_probe(ckey(parent, tok));
   wsync();
   if (lane0()) {
@@ -374,6 +428,16 @@ E2_DNI void child_erase(u32 parent, i32 tok) {
 // warp-wide: erase the entry at a known position (the node's ctpos);
 // falls back to a probe if the position does not hold the key.
 E2_DNI void child_erase_at(u32 pos, u32 parent, i32 tok) {
+  if (pos == kCtInline) {
+    NodeRec* rp = nget(parent);
+    wsync();
+    if (lane0() && rp->in_tok == tok && rp->in_slot != 0) {
+      rp->in_slot = 0;
+      rp->in_tok = 0;
+    }
+    wsync();
+    return;
+  }
   const u64 key = ckey(parent, tok);
   if ((u64)pos <= DEV.ct_mask && DEV.ct[pos].key == key) {
     if (lane0()) DEV.ct[pos].key = kTombKey;
@@ -871,10 +935,18 @@ E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
   }
   wsync();
   // the parent's entry for this edge now leads to the prefix (which copied
-  // the record, ctpos included); the suffix hangs under the prefix
-  if (lane0()) DEV.ct[hs.ctpos].val = q;
+  // the record, ctpos included); the suffix hangs under the prefix as its
+  // inline child (no table entry)
+  if (lane0()) {
+    if (hs.ctpos == kCtInline)
+      npoke(hs.parent)->in_slot = q;
+    else
+      DEV.ct[hs.ctpos].val = q;
+    rq->in_tok = tok_k;
+    rq->in_slot = s;
+    rs->ctpos = kCtInline;
+  }
   wsync();
-  child_insert(q, tok_k, s);
   if (!rekey) return q;
   // LRU: the suffix inherits the leaf role under its new id.
   u64 m = hs.cmask;
@@ -911,6 +983,18 @@ E2_DNI u32 new_leaf(u32 parent, i64 off, u32 len, u32 depth) {
     ndirty(rp);
   }
   wsync();
+#if E2_WARP
+  if (g_defer_ct && threadIdx.x < 32 && rp->in_slot != 0) {
+    if (lane0()) {
+      g_ctd.parent = parent;
+      g_ctd.child = l;
+      g_ctd.tok = t0;
+      g_ctd.pending = 1;
+    }
+    wsync();
+    return l;
+  }
+#endif
   child_insert(parent, t0, l);
   return l;
 }

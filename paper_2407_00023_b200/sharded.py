@@ -96,6 +96,12 @@ class ShardedReplay:
         if rc != abi.E2_OK:
             raise RuntimeError(self.lib.e2_last_error(self.h).decode())
 
+    def _settle(self):
+        """Collectives complete on the device asynchronously; the library's
+        next step reads their output on its own stream: wait for them."""
+        if self.torch.device(self.device).type == "cuda":
+            self.torch.cuda.current_stream(self.device).synchronize()
+
     def _all_gather(self, send, nbytes):
         import torch.distributed as dist
 
@@ -136,6 +142,7 @@ class ShardedReplay:
             send = self.send.get(slice_bytes)
             self._check(lib.e2_shard_match(h, lo, cnt, p(send)))
             recv = self._all_gather(send, slice_bytes)
+            self._settle()
             if rank == 0:
                 rc = lib.e2_shard_commit(h, p(recv), per, ctypes.byref(db))
                 if rc != abi.E2_OK:
@@ -153,6 +160,7 @@ class ShardedReplay:
                 self._check(lib.e2_shard_delta_copy(h, p(delta)))
             if world > 1:
                 dist.broadcast(delta, 0)
+                self._settle()
             if rank != 0:
                 self._check(lib.e2_shard_apply(h, p(delta), size))
             self.batches += 1
@@ -202,7 +210,8 @@ def bench_main(args, metric, unit, config_dict, clock_sampler):
     n, G = trace.n, cfg.n_gpus
     drv = DriverConfig(**{**cfg.driver.__dict__, "batch": args.batch})
     sched = GlobalScheduler(G, cfg.sched, policy=cfg.policy, lib=lib)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # the library and the timing events share it
+    torch.cuda.set_stream(stream)     # the collectives order against it too
     lib.e2_set_stream(sched._h, ctypes.c_void_p(stream.cuda_stream))
     tens = trace_tensors(trace, dev)
     rep = ShardedReplay(sched, tens, drv, dev, rank, ws, want_costs=True)

@@ -10,7 +10,7 @@ cfg = W.CONFIGS[name]
 tr = cfg.trace(lib=lib, n_requests=n)
 s = GlobalScheduler(cfg.n_gpus, cfg.sched, lib=lib)
 r = s.replay(tr, cfg.driver)
-buf = (ctypes.c_uint64 * 40)()
+buf = (ctypes.c_uint64 * 48)()
 lib.e2_debug_phases(s._h, buf)
 names = ["redirects", "decide_other", "commit_other", "decision_out", "evict_apply", "finished", "walk", "cost_prep",
          "cost_pick", "ensure_path", "path_update", "evict_plan", "", "", "", ""]
@@ -19,4 +19,7 @@ print(name, n, "cycles/request total %.0f" % (tot / n), " ".join("%s=%.0f" % (na
       "| warp1: fix_wait=%.0f fixes=%.0f evict=%.0f out=%.0f spin=%.0f books=%.0f" % tuple(buf[k] / n for k in (31, 20, 21, 22, 29, 19)),
       "| evict: plan=%.0f tail_pre=%.0f split=%.0f tail_post=%.0f whole=%.0f" % tuple(buf[k] / n for k in (24, 28, 25, 26, 27)),
       "| decide: prologue=%.0f cands=%.0f | validate=%.0f handoff=%.0f hint_row=%.0f post=%.0f" % tuple(buf[k] / n for k in (32, 33, 34, 35, 36, 37)),
-      "| per request: walk_fallback_probes=%.3f evict_tail=%.3f evict_whole=%.3f" % (buf[12] / n, buf[13] / n, buf[14] / n))
+      "| per request: walk_fallback_probes=%.3f evict_tail=%.3f evict_whole=%.3f" % (buf[12] / n, buf[13] / n, buf[14] / n),
+      "| walk: hinted=%.0f leader_switch=%.0f climb=%.0f probes=%.0f extents=%.0f" % tuple(buf[k] / n for k in (38, 39, 40, 41, 6)),
+      "| redo: spec_fail=%.4f conflict=%.4f" % (buf[42] / n, buf[43] / n),
+      "| explore: ratios=%.0f prepare=%.0f costs=%.0f" % (buf[46] / n, buf[44] / n, buf[45] / n))

@@ -42,7 +42,9 @@ def _worker(rank, ws, port, lib_path, out_dir, cfg_name, n_req, batch, device="c
     dev = torch.device(device)
     if dev.type == "cuda":
         torch.cuda.set_device(dev)
-        lib.e2_set_stream(s._h, torch.cuda.current_stream(dev).cuda_stream)
+        st = torch.cuda.Stream(dev)
+        torch.cuda.set_stream(st)
+        lib.e2_set_stream(s._h, st.cuda_stream)
     rep = sharded.ShardedReplay(s, sharded.trace_tensors(trace, dev), drv, dev, rank, ws)
     digests = []
 
