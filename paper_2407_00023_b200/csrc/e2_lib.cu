@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride
   }
   if (threadIdx.x == 0) ncand = 0;
   __syncthreads();
-  for (i64 w = threadIdx.x; w < nrows; w += blockDim.x) {
+  // a sample of the rows is enough to rank the root's children by use
+  const i64 step = nrows > 4096 ? nrows / 4096 : 1;
+  for (i64 w = (i64)threadIdx.x * step; w < nrows; w += (i64)blockDim.x * step) {
     const u32 v = rows[w * (i64)hstride];
     if (v == kNil || v == kRoot || v >= g_dev.node_cap) continue;
     u32 h = (u32)(mix64(v) & (kTopSet - 1));
@@ -268,7 +270,13 @@ __global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride
     e.pad = 0;
     e.edge_off = r->edge_off;
     ents[pos] = e;
-    for (u32 k = 0; k < hl; ++k) ((i32*)(img + e.head_off))[k] = g_dev.tok[r->edge_off + k];
+  }
+  __syncthreads();
+  // the heads, every thread of the block per entry
+  for (u32 j = 0; j < ne; ++j) {
+    const TopEnt e = ents[j];
+    for (u32 k = threadIdx.x; k < e.head_len; k += blockDim.x)
+      ((i32*)(img + e.head_off))[k] = g_dev.tok[e.edge_off + k];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -306,9 +314,9 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32, kMatchBlocksPerSM)
       mbar_expect_tx(&top_bar, tb);
       bulk_g2s(top, top_img, tb, &top_bar);
     }
-    __syncthreads();
-    mbar_wait(&top_bar, 0);
+    __syncthreads();  // the barrier is initialised; each warp waits on it at its first lookup
   }
+  bool top_ready = !staged;
   unsigned long long acc = 0;
   unsigned int w = 0;
   if (lane0()) w = atomicAdd(next, (unsigned)kTile);
@@ -323,6 +331,10 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32, kMatchBlocksPerSM)
       if (lane() < kTile && q < n && len[base + q] > 0) key = g_dev.tok[off[base + q]];
       const u32 grp = __match_any_sync(0xffffffffu, key);
       const int lead = ffs32(grp);
+      if (!top_ready) {  // the bulk copy overlapped this warp's first loads
+        mbar_wait(&top_bar, 0);
+        top_ready = true;
+      }
       if (lane() == lead && key >= 0) ent = top_find(top, key);
       ent = shfl(ent, lead);
     }
@@ -337,8 +349,8 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32, kMatchBlocksPerSM)
         dslot[q] = m.div_slot;
         dm[q] = m.div_m;
         if (m.levels >= hstride) atomicMax(max_levels, (unsigned int)min_<i64>(m.levels, 0x7fffffff));
+        acc += (unsigned long long)m.bytes;
       }
-      acc += (unsigned long long)m.bytes;
     }
     w = shfl(wn, 0);
   }
@@ -346,7 +358,7 @@ __global__ void __launch_bounds__(kMatchWarpsPerBlock * 32, kMatchBlocksPerSM)
   __shared__ unsigned long long blk_bytes;
   if (threadIdx.x == 0) blk_bytes = 0;
   __syncthreads();
-  if (lane0()) atomicAdd(&blk_bytes, acc);
+  if (acc) atomicAdd(&blk_bytes, acc);  // the lanes that counted requests
   __syncthreads();
   if (threadIdx.x == 0) atomicAdd(bytes, blk_bytes);
 }

@@ -77,6 +77,7 @@ def test_streamed_replay_equals_one_replay_hostsim(hostsim_lib, ref_lib, gen_lib
 
 @pytest.mark.gpu
 def test_streamed_c5_parity_b200(b200_lib, ref_lib, gen_lib):
-    """C5 as streamed on the B200: 2 chunks of 65536 (131072 requests) vs the
-    reference replaying the concatenation in one go."""
-    _stream_parity(b200_lib, ref_lib, gen_lib, _small_stream(131072, 65536))
+    """C5 as streamed on the B200: 3 chunks of 16384 vs the reference
+    replaying the concatenation in one go (C5 at 100k requests in one replay:
+    test_parity.py)."""
+    _stream_parity(b200_lib, ref_lib, gen_lib, _small_stream(3 * 16384, 16384))
