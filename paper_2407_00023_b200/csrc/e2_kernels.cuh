@@ -505,6 +505,9 @@ struct Pipe {
   volatile long long ready;
   volatile long long books_done;  // warp 3: bookkeeping of requests [0, books_done) applied
   volatile long long fix_ready;   // warp 0: request fix_ready-1's path is updated (LRU fixes may start)
+  volatile long long commit_done; // warp 0: request commit_done-1 is fully committed (FIFO driver)
+  volatile long long w1_fixed;    // warp 1: done with the scratch of requests < w1_fixed (out + fixes)
+  i32 c_ok;                       // the request handed to warp 1 commits (else warp 1 does not evict)
   const Scr* fs;                  // that request's scratch (deferred LRU fixes)
   i32 fg;                         // and instance
   i64 c_id, c_cached, c_n;
@@ -523,6 +526,24 @@ E2_D void wait_pause() {
 // bar.sync is the .aligned barrier: the whole warp must arrive converged,
 // and the flag polls before it let lanes leave their loops on different
 // iterations (compute-sanitizer synccheck), so reconverge first.
+// While warp 0 waits at barrier 1: L1 prefetches for the commit of the
+// request it just decided speculatively — the per-instance parts of the
+// path's records (last_access, hits, cached-child counts: the path update
+// reads them) and the edge token at the split point (ensure_path).
+E2_D void prefetch_commit(const Scr* s, const Walk& w) {
+  const int np = min_(s->npath, kMaxPath);
+  const u32 rs = DEV.rs;
+  for (int l = lane(); l < np; l += kWidth) {
+    const char* rec = (const char*)grec(PSLOT(s, l));
+    if (rs > 128) pf(rec + 128);
+    if (rs > 256) pf(rec + 256);
+  }
+  if (lane0() && w.ok && w.last != kRoot) {
+    const NodeRec* r = npeek(w.last);
+    if (w.last_m < (i64)r->edge_len) pf(DEV.tok + r->edge_off + w.last_m);
+  }
+}
+
 E2_D void bar_pair(int id) {
   __syncwarp();
   asm volatile("barrier.sync %0, 64;" ::"r"(id) : "memory");
@@ -699,21 +720,34 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
     Dec pdec;
     const Scr* psb = nullptr;
     PHASE_MARK1(23);
+    // the evictions of request ci start as soon as warp 0's path update of
+    // ci is done (the LRU fixes before them); the rest of warp 0's commit
+    // (path log, window slot, hint row) touches nothing an eviction reads.
+    // The criterion-7 FIFO driver reads request ci's tail slot, written at
+    // the very end of the commit: there the evictions wait for commit_done.
+    const bool early = a.eviction != E2_EVICT_FIFO_TAIL;
     for (i64 ci = 0;; ++ci) {
       bar_pair(1);
       PHASE_MARK1(23);  // waiting
       if (have) replay_out(psb, a, pli, pdec);
       PHASE_MARK1(22);  // decision record
-      // the LRU re-indexing of the path warp 0 is committing, beside the
-      // rest of its commit (it must precede this warp's evictions)
       while (pp->fix_ready != ci + 1 && !*(volatile i32*)&pp->stop) wait_pause();
       acquire_after_poll();
       PHASE_MARK1(31);  // waiting for warp 0's path update
-      if (pp->fix_ready == ci + 1 && pp->fs->fix_D > 0) path_lru_fix(pp->fs, pp->fs->fix_D, pp->fg);
+      bool go = pp->fix_ready == ci + 1 && !*(volatile i32*)&pp->stop;
+      if (go && pp->fs->fix_D > 0) path_lru_fix(pp->fs, pp->fs->fix_D, pp->fg);
       PHASE_MARK1(20);  // LRU fixes
-      bar_pair(2);
-      PHASE_MARK1(23);
-      if (pp->stop) {
+      if (lane0()) {
+        __threadfence_block();
+        pp->w1_fixed = ci + 1;  // warp 0 may reuse the scratch buffers
+      }
+      wsync();
+      if (go && !early) {
+        while (pp->commit_done != ci + 1 && !*(volatile i32*)&pp->stop) wait_pause();
+        acquire_after_poll();
+        go = pp->commit_done == ci + 1;
+      }
+      if (!go || !pp->c_ok || *(volatile i32*)&HOT.err) {
         if (g_ctd.pending) {  // the failing request's leaf: keep the table consistent
           child_insert(g_ctd.parent, g_ctd.tok, g_ctd.child);
           if (lane0()) g_ctd.pending = 0;
@@ -723,7 +757,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       }
       if (lane0()) g_ntouch = 0;
       wsync();
-      if (g_ctd.pending) {  // warp 0's deferred child-table insert of request pp->li's leaf
+      if (g_ctd.pending) {  // warp 0's deferred child-table insert of request ci's leaf
         child_insert(g_ctd.parent, g_ctd.tok, g_ctd.child);
         if (lane0()) g_ctd.pending = 0;
         wsync();
@@ -736,10 +770,10 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       replay_evict(a, pp->li, pp->g);
       PHASE_MARK1(21);  // evictions
     }
+    bar_pair(2);  // final rendezvous: warp 0 waits for the last decision record
     return;
   }
   i64 i = 0, fail = -1;
-  bool past1 = false;  // warp 0 is between barrier 1 and barrier 2
   bool pre_done = false;  // warp 1 ran this request's replay_pre
   for (; i < a.n; ++i) {
     Scr* s = s2 + (i & 1);  // warp 1 reads the other buffer (request i-1) meanwhile
@@ -750,6 +784,11 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       while (pp->books_done < i) wait_pause();
       acquire_after_poll();
       PHASE(30);  // waiting for warp 3's bookkeeping
+      // warp 1 finished reading the scratch this request reuses (request
+      // i-2's decision record, request i-1's LRU fixes)
+      while (pp->w1_fixed < i) wait_pause();
+      acquire_after_poll();
+      PHASE(18);  // waiting for warp 1's LRU fixes / decision record
     }
     const double now = pre_done ? s->pre_now : replay_pre(s, a, i);
     // decide speculatively while warp 1 evicts for request i-1
@@ -761,9 +800,9 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       dec = decide(s, DEV.tok + a.off[r], a.len[r], a.L[i], a.hint + i * a.hstride, a.hstride, a.S[i], now, w, true,
                    a.lead ? a.lead + i : nullptr, a.hint);
     }
+    if (specd && !s->spec_bad) prefetch_commit(s, w);
     PHASE(1);
     bar_pair(1);
-    past1 = true;
     PHASE(16);  // waiting for the previous request's eviction
     if (HOT.err) {  // evict(i-1) failed
       fail = i - 1;
@@ -821,6 +860,12 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
         pp->fs = s;
         pp->fg = dec.gpu;
         s->fix_D = 0;  // nothing to re-index unless path_update_par defers it
+        // what warp 1 needs for this request's decision record and evictions
+        pp->li = i;
+        pp->g = dec.gpu;
+        pp->dec = dec;
+        pp->s = s;
+        pp->c_ok = dec.ok ? 1 : 0;
       }
       wsync();
       ok = dec.ok && replay_main(s, a, i, now, dec, &w, E2_DEFER_LRU, defer, E2_DEFER_LRU ? &pp->fix_ready : nullptr);
@@ -846,21 +891,16 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       break;
     }
     if (lane0()) {
-      pp->li = i;
-      pp->g = dec.gpu;
-      pp->stop = 0;
-      pp->dec = dec;
-      pp->s = s;
+      __threadfence_block();
+      pp->commit_done = i + 1;
     }
     wsync();
     PHASE(37);
-    bar_pair(2);
-    PHASE(18);  // waiting for warp 1's LRU fixes / decision record
-    past1 = false;
   }
-  if (!past1) bar_pair(1);  // wait for the last evict
+  if (fail < 0) bar_pair(1);  // wait for the last evict
   if (HOT.err && fail < 0) fail = a.n - 1;  // the last evict failed
   if (lane0()) {
+    __threadfence_block();
     pp->stop = 1;
     g_pf_stop = 1;
   }

@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
     pipe.ready = 0;
     pipe.books_done = 0;
     pipe.fix_ready = 0;
+    pipe.commit_done = 0;
+    pipe.w1_fixed = 0;
+    pipe.c_ok = 0;
     pipe.stop = 0;
     ss[0].win_done = ss[1].win_done = 0;
   }
