@@ -211,6 +211,8 @@ int e2_window_sizes(e2_handle* h, int32_t gpu, double now, int64_t* n_scheduled,
  *
  *   for i in arrival order:
  *     now = max(now, arrival[i])
+ *     while prune_interval_ms > 0 and next_tick <= now:
+ *       prune_dead_nodes(next_tick); next_tick += prune_interval_ms
  *     d = schedule_request(r_i, now)
  *     if prefill_cached: note_prefill_cached(p_i, d.gpu, now)
  *     eviction == FIFO_TAIL: push (i, |p_i| - trunk_len) on fifo[d.gpu];
@@ -234,6 +236,10 @@ typedef struct {
   int64_t high_water;
   int64_t finish_lag;
   int64_t batch; /* requests per device batch (0 = implementation default) */
+  /* > 0: before a request at `now`, prune_dead_nodes(T) for every tick
+   * T = k * prune_interval_ms (k = 1, 2, ...) with T <= now, in order — the
+   * simulator's RebalanceTick cadence (simulator.cpp:217-229, H/2). */
+  double prune_interval_ms;
 } e2_driver_cfg;
 
 /* Host buffers: tokens (CSR, offsets[n+1]), ids, arrivals, output_lens.

@@ -1159,10 +1159,16 @@ int e2_replay(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const
   int64_t* ft = (int64_t*)malloc(8 * (size_t)(n + 1) * (size_t)G);
   int64_t fh[E2_MAX_GPUS] = {0}, fn[E2_MAX_GPUS] = {0};
   double now = 0;
+  double tick = drv->prune_interval_ms > 0 ? drv->prune_interval_ms : 0;
   int rc = 0;
   int64_t i;
   for (i = 0; i < n; ++i) {
     if (arrivals[i] > now) now = arrivals[i];
+    while (tick > 0 && tick <= now) { /* prune ticks (simulator.cpp:217-229) */
+      int64_t removed = 0;
+      e2_prune_dead_nodes(h, tick, &removed);
+      tick += drv->prune_interval_ms;
+    }
     const int32_t* p = tokens + offsets[i];
     int64_t len = offsets[i + 1] - offsets[i];
     Match mm = walk(h, p, len);

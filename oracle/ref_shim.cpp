@@ -412,10 +412,15 @@ int e2_replay(e2_handle* h, const int32_t* tokens, const int64_t* offsets, const
   GlobalScheduler& s = *h->s;
   std::vector<std::deque<std::pair<int64_t, int64_t>>> fifo(h->n);
   double now = 0;
+  double tick = drv->prune_interval_ms > 0 ? drv->prune_interval_ms : 0;
   int64_t i = 0;
   int rc = guard(h, [&] {
     for (i = 0; i < n; ++i) {
       now = std::max(now, arrivals[i]);
+      while (tick > 0 && tick <= now) {  // the simulator's prune ticks (simulator.cpp:217-229)
+        s.prune_dead_nodes(tick);
+        tick += drv->prune_interval_ms;
+      }
       Request r;
       r.id = ids[i];
       r.arrival_ms = arrivals[i];
@@ -481,10 +486,15 @@ int e2ref_time_loop(e2_handle* h, const int32_t* tokens, const int64_t* offsets,
   auto t0 = std::chrono::steady_clock::now();
   int rc = guard(h, [&] {
     SimTime now = 0;
+    double tick = drv->prune_interval_ms > 0 ? drv->prune_interval_ms : 0;
     t0 = std::chrono::steady_clock::now();
     for (i = 0; i < n; ++i) {
       const Request& r = reqs[i];
       now = std::max(now, r.arrival_ms);
+      while (tick > 0 && tick <= now) {
+        s.prune_dead_nodes(tick);
+        tick += drv->prune_interval_ms;
+      }
       const Decision d = s.schedule_request(r, now);
       if (drv->prefill_cached) s.note_prefill_cached(r.prompt, d.gpu, now);
       if (drv->eviction == E2_EVICT_FIFO_TAIL) {

@@ -127,6 +127,7 @@ class DriverCfg(ctypes.Structure):
         ("high_water", ctypes.c_int64),
         ("finish_lag", ctypes.c_int64),
         ("batch", ctypes.c_int64),
+        ("prune_interval_ms", ctypes.c_double),
     ]
 
 

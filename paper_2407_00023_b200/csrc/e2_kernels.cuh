@@ -800,7 +800,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       dec = decide(s, DEV.tok + a.off[r], a.len[r], a.L[i], a.hint + i * a.hstride, a.hstride, a.S[i], now, w, true,
                    a.lead ? a.lead + i : nullptr, a.hint);
     }
-    if (specd && !s->spec_bad) prefetch_commit(s, w);
+    if (specd && !s->spec_bad && s->spec_walked) prefetch_commit(s, w);  // only after a complete walk
     PHASE(1);
     bar_pair(1);
     PHASE(16);  // waiting for the previous request's eviction

@@ -636,6 +636,10 @@ struct ReplaySession {
   i64 n = 0, B = 0, next_b0 = 0, cur_b = 0, done = 0;
   i64 cb0 = 0, cnb = 0;  // the current batch
   i64 carried = 0;       // streamed replay: requests of the previous chunk at the front of the arrays
+  // prune ticks (driver prune_interval_ms): (combined request index it
+  // precedes, tick time); batches are cut at these indices
+  std::vector<std::pair<i64, double>> ticks;
+  size_t tick_pos = 0;
   SerialArgs a;
   e2_decision* out = nullptr;  // caller's buffers
   e2_cost* costs = nullptr;
@@ -744,6 +748,7 @@ struct e2_handle {
   // arrivals and output lengths are carried so their note_finished calls
   // land in the next chunk exactly where a single replay would make them
   bool cont = false;
+  double next_tick = 0;  // streamed replays: the next prune tick (driver prune_interval_ms)
   i64 prev_total = 0;   // requests replayed since the last reset
   i64 carry_n = 0;
   i64 *carry_ids = nullptr, *carry_out = nullptr;
@@ -1912,6 +1917,7 @@ int e2_reset(e2_handle* h) {
     h->queue_stats.clear();
     h->prev_total = 0;
     h->carry_n = 0;
+    h->next_tick = 0;
   });
 }
 
@@ -2361,6 +2367,26 @@ void replay_begin(e2_handle* h, const int32_t* tokens, const int64_t* offsets, c
     d_arr = h->cb_arr;
     d_out = h->cb_out;
   }
+  // prune ticks: the simulator's cadence on the driver clock
+  if (drv->prune_interval_ms > 0) {
+    std::vector<double> arr_h((size_t)n);
+    if (device_ptrs) {
+      d2h(arr_h.data(), arrivals, (size_t)n * 8, h->stream);
+      ssync(h->stream);
+    } else {
+      memcpy(arr_h.data(), arrivals, (size_t)n * 8);
+    }
+    double now = cont ? h->hot.drv_now : 0.0;
+    double t = cont ? h->next_tick : drv->prune_interval_ms;
+    for (i64 i = 0; i < n; ++i) {
+      now = std::max(now, arr_h[(size_t)i]);
+      while (t <= now) {
+        S.ticks.push_back({C + i, t});
+        t += drv->prune_interval_ms;
+      }
+    }
+    h->next_tick = t;
+  }
   // driver state (a streamed continuation keeps the driver clock)
   if (!cont) {
     h->hot.drv_now = 0;
@@ -2413,9 +2439,16 @@ bool replay_next(e2_handle* h) {
     S.cnb = 0;
     return false;
   }
+  // prune ticks due before this batch's first request (prune_dead_nodes at
+  // the tick time; a batch never spans a tick, so K1 matches the pruned tree)
+  while (S.tick_pos < S.ticks.size() && S.ticks[S.tick_pos].first <= S.next_b0) {
+    run_simple(h, OP_PRUNE_DEAD, 0, 0, S.ticks[S.tick_pos].second);
+    S.tick_pos++;
+  }
   S.cb0 = S.next_b0;
   S.cnb = std::min<i64>(S.cur_b, S.n - S.next_b0);
-  S.next_b0 += S.cur_b;
+  if (S.tick_pos < S.ticks.size()) S.cnb = std::min<i64>(S.cnb, S.ticks[S.tick_pos].first - S.next_b0);
+  S.next_b0 += S.cnb;
   S.cur_b = std::min<i64>(S.B, S.cur_b * 2);
   reserve_batch(h, S.cnb);
   return true;
@@ -2727,6 +2760,7 @@ int e2_shard_begin(e2_handle* h, const int32_t* d_tokens, const int64_t* d_offse
     if (world < 1 || rank < 0 || rank >= world) throw Fail(E2_ERR_ARG, "shard: bad rank/world");
     if (n <= 0) throw Fail(E2_ERR_ARG, "shard: empty trace");
     if (h->cont) throw Fail(E2_ERR_ARG, "shard: streamed continuation is not supported");
+    if (drv->prune_interval_ms > 0) throw Fail(E2_ERR_ARG, "shard: prune ticks inside a sharded replay are not supported");
     h->sh.on = true;
     h->sh.rank = rank;
     h->sh.world = world;

@@ -461,8 +461,10 @@ class DriverConfig:
     high_water: int = 150000
     finish_lag: int = 2000
     batch: int = 0
+    prune_interval_ms: float = 0.0  # > 0: prune_dead_nodes at every tick k*interval <= now (simulator cadence H/2)
 
     def to_c(self) -> abi.DriverCfg:
         return abi.DriverCfg(
-            self.eviction, int(self.prefill_cached), self.trunk_len, self.high_water, self.finish_lag, self.batch
+            self.eviction, int(self.prefill_cached), self.trunk_len, self.high_water, self.finish_lag, self.batch,
+            float(self.prune_interval_ms),
         )

@@ -18,14 +18,15 @@ from paper_2407_00023_b200.scheduler import DriverConfig, GlobalPolicy, Schedule
 from parity import assert_same_state, diff_decisions, replay
 
 
-def _cfg(name, arch, n, G, cap, hw, evict, H=10000.0, batch=0, trunk=0, policy=None, **over):
+def _cfg(name, arch, n, G, cap, hw, evict, H=10000.0, batch=0, trunk=0, policy=None, prune=0.0, **over):
     c = W.Config(
         name,
         arch,
         n,
         G,
         SchedulerConfig(kv_capacity_tokens=cap, history_window_ms=H),
-        DriverConfig(eviction=evict, trunk_len=trunk, high_water=hw, finish_lag=min(2000, n // 4), batch=batch),
+        DriverConfig(eviction=evict, trunk_len=trunk, high_water=hw, finish_lag=min(2000, n // 4), batch=batch,
+                     prune_interval_ms=prune),
         spec_overrides=over,
     )
     c.policy = policy
@@ -52,6 +53,11 @@ CASES = {
                                policy=GlobalPolicy(rebalance=False, pd_balance=False)),
     "short_window": _cfg("shortH", "doc_qa", 1200, 8, 60000, 57000, LRU, H=300.0),
     "c4_3k": dataclasses.replace(W.CONFIGS["c4"], n_requests=3000),
+    # dead-node pruning at the simulator's H/2 cadence inside the replay (simulator.cpp:217-229)
+    "prune_toolbench": _cfg("prune_tb", "toolbench", 2500, 4, 30000, 22000, LRU, H=200.0, batch=300, prune=100.0),
+    "prune_tot": _cfg("prune_tot", "tree_of_thought", 2500, 8, 20000, 19000, LRU, H=150.0, batch=256, prune=75.0),
+    "prune_embodied": _cfg("prune_emb", "embodied_agent", 1500, 4, 30000, 28500, LRU, H=100.0, prune=50.0),
+    "prune_fifo": _cfg("prune_fifo", "toolbench", 1500, 4, 60000, 45000, FIFO, H=120.0, trunk=1860, prune=60.0),
     "c5_3k": W.MixConfig(**{f.name: getattr(W.CONFIGS["c5"], f.name) for f in dataclasses.fields(W.Config)
                             if f.name != "n_requests"}, n_requests=3000),
 }
