@@ -562,6 +562,8 @@ def main():
                     help="requests of the trace the host reference is timed on (0 = all)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-traffic", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)  # gloo: dev check on one GPU
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--probe-n", type=int, default=120000, help=argparse.SUPPRESS)
     args = ap.parse_args()

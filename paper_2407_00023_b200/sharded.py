@@ -201,9 +201,15 @@ def bench_main(args, metric, unit, config_dict, clock_sampler):
     from . import workload
 
     ws, rank, local = dist_env()
+    if getattr(args, "same_device", False):
+        local = 0  # dev check of the N>1 path on a one-GPU box (with --dist-backend gloo)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    backend = getattr(args, "dist_backend", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
     cfg = workload.CONFIGS[args.config]
     lib = abi.product_lib()
     trace = cfg.trace(lib=lib)
