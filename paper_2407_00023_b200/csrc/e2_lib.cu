@@ -299,7 +299,10 @@ __global__ void __launch_bounds__(1024) k_top_build(const u32* rows, int hstride
 // (one TMA bulk copy).  A tile's level-0 lookups are deduplicated: lanes
 // holding the same first token form a __match_any_sync group and only its
 // lowest lane searches the staged table.
-constexpr int kMatchBlocksPerSM = 4;
+#ifndef E2_K1_BLOCKS
+#define E2_K1_BLOCKS 4
+#endif
+constexpr int kMatchBlocksPerSM = E2_K1_BLOCKS;
 #ifndef E2_K1_TILE
 #define E2_K1_TILE 2
 #endif

@@ -122,7 +122,10 @@ E2_D i64 warp_lcp(const i32* a, const i32* b, i64 lim) {
 // memory; every K1 block copies it into shared memory with one TMA bulk copy
 // (cp.async.bulk + mbarrier complete_tx).  Level 0 of a walk then costs no
 // child-table probe and compares the head of its edge from shared memory.
-constexpr u32 kTopBytes = 32 * 1024;
+#ifndef E2_TOP_KB
+#define E2_TOP_KB 32
+#endif
+constexpr u32 kTopBytes = E2_TOP_KB * 1024;
 constexpr u32 kTopMaxEnt = 254;
 constexpr u32 kTopHeadMax = 2048;  // tokens staged per root child at most
 struct TopHdr {

@@ -30,3 +30,18 @@ def test_dropin_hostsim():
     out = subprocess.run([exe, "3000"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "drop-in OK" in out.stdout
+
+
+@pytest.mark.gpu
+def test_dropin_b200():
+    """The same lock-step loop with the drop-in on libe2sched.so (prebuilt by
+    `make -C oracle e2e` where the reference sources are)."""
+    exe = os.path.join(REPO, "oracle", "_ref", "drop_in_b200")
+    if os.path.isdir(REF):
+        subprocess.run(["make", "-s", "_ref/drop_in_b200"], cwd=os.path.join(REPO, "oracle"), check=True)
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/drop_in_b200 not built")
+    out = subprocess.run([exe, "3000"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "drop-in OK" in out.stdout and "b200 backend" in out.stdout
+    print(out.stdout.strip().splitlines()[-1])
