@@ -292,6 +292,13 @@ E2_HD i64 plan_eviction(int g, i64 need, bool partial, Visit&& visit) {
   u64* s_id = DEV.scr_id + (u64)g * DEV.scap;
   i64* s_val = DEV.scr_val + (u64)g * DEV.scap;
   u32 ns = 0, nsurf_head = 0, nsim = 0;
+  // simulated cached-child counts of the parents met so far: the first kLin
+  // in a list (short plans: a few L1-resident compares), the rest in an
+  // open-addressing table keyed (plan generation << 32 | slot), so keys of
+  // earlier plans read as empty and the table needs no clearing
+  constexpr u32 kLin = 16;
+  const u64 tmask = (u64)((DEV.scap - half) / 2) - 1;  // table entries: a power of two below scap - half - kLin
+  u64 gen = 0;  // taken when the table is first used by this plan
   const u32 nd = HOT.dir_n[g];
   u32 k = 0, j = 0, page = kNil;
   i32 pcnt = 0;
@@ -342,18 +349,35 @@ E2_HD i64 plan_eviction(int g, i64 need, bool partial, Visit&& visit) {
     if (p != kNil && p != kRoot) {
       const NodeRec* rp = npeek(p);
       if (!rcached(rp, g)) continue;
-      u32 xi = 0;
-      while (xi < nsim && s_slot[half + xi] != p) ++xi;
+      const u32 nlin = min_(nsim, kLin);
+      u64 xi = 0;
+      while (xi < nlin && s_slot[half + xi] != p) ++xi;
+      bool found = xi < nlin;
+      if (!found && nsim >= kLin) {
+        if (gen == 0) gen = ++s_la[half];  // this instance's plan counter (s_la's upper half is unused)
+        const u64 key = (gen << 32) | (u64)p;
+        u64 h = mix64((u64)p) & tmask;
+        for (;;) {
+          const u64 kk = s_id[half + kLin + h];
+          if (kk == key || (kk >> 32) != gen) break;  // found, or a free entry (another plan's key)
+          h = (h + 1) & tmask;
+        }
+        xi = kLin + h;
+        found = s_id[half + xi] == key;
+        if (!found) {
+          if ((u64)(nsim - kLin) * 2 >= tmask + 1) {
+            set_err(kErrCapacity, kWhyScratchCap);
+            break;
+          }
+          s_id[half + xi] = key;
+        }
+      }
       i64 c;
-      if (xi < nsim) {
+      if (found) {
         c = s_val[half + xi] - 1;
       } else {
-        if (nsim >= DEV.scap - half) {
-          set_err(kErrCapacity, kWhyScratchCap);
-          break;
-        }
         c = (i64)rccc(rp, G)[g] - 1;
-        s_slot[half + nsim] = p;
+        if (nsim < kLin) s_slot[half + nsim] = p;  // xi == nsim: the list's next entry
         nsim++;
       }
       s_val[half + xi] = c;
