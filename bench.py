@@ -211,6 +211,10 @@ def run_reference_arm(args):
     return 0
 
 
+def eff_batch(args, cfg) -> int:
+    return args.batch or cfg.driver.batch or 16384
+
+
 def _config_dict(cfg, n, args, ws):
     return {
         "workload": cfg.name,
@@ -222,7 +226,7 @@ def _config_dict(cfg, n, args, ws):
         "finish_lag": cfg.driver.finish_lag,
         "kv_capacity": cfg.sched.kv_capacity_tokens,
         "history_window_ms": cfg.sched.history_window_ms,
-        "batch": args.batch,
+        "batch": eff_batch(args, cfg),
         "parallelism": f"sharded{ws} (K1 sharded, commit on rank 0, NCCL delta broadcast)" if ws > 1 else "single",
         "l2": "inputs larger than L2 (prompt arena > 126 MB), no flush",
     }
@@ -247,7 +251,7 @@ def measure_traffic(args, cfg, timeout=420):
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
            "--clock-control", "none", "-k", "regex:k_serial|k_match", "--launch-skip", str(2 * skip),
            "--launch-count", "4", "--csv", sys.executable, os.path.abspath(__file__), "--probe",
-           "--config", args.config, "--probe-n", str(args.probe_n), "--batch", str(args.batch)]
+           "--config", args.config, "--probe-n", str(args.probe_n), "--batch", str(eff_batch(args, cfg))]
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
     except Exception:
@@ -278,7 +282,7 @@ def measure_traffic(args, cfg, timeout=420):
     if not res:
         return None
     # the probe's full-size batches hold args.batch requests per launch
-    return {k: {"dram_bytes_per_launch": statistics.mean(b for b, _ in v), "requests_per_launch": args.batch,
+    return {k: {"dram_bytes_per_launch": statistics.mean(b for b, _ in v), "requests_per_launch": eff_batch(args, cfg),
                 "ncu_launch_s": statistics.mean(t for _, t in v if t), "launches": len(v)} for k, v in res.items()}
 
 
@@ -288,7 +292,7 @@ def run_probe(args):
     lib = abi.product_lib()
     trace = cfg.trace(lib=lib, n_requests=args.probe_n)
     drv = cfg.driver
-    drv.batch = args.batch
+    drv.batch = eff_batch(args, cfg)
     s = GlobalScheduler(cfg.n_gpus, cfg.sched, policy=cfg.policy, lib=lib)
     r = s.replay(trace, drv, want_costs=False)
     assert r.n_done == trace.n
@@ -407,7 +411,7 @@ def secondary_lines(args, dev):
                                                   finish_lag=2000))):
         cfg = workload.Config(base.name, base.archetype, base.n_requests, base.n_gpus, base.sched, drv)
         trace = cfg.trace()
-        rep = DeviceReplay(cfg, trace, dev, args.batch)
+        rep = DeviceReplay(cfg, trace, dev, eff_batch(args, cfg))
         ms, _ = _timed_steps(rep, 3, 2)
         rep.close()
         line = {"workload": cfg.name, "eviction": label, "requests": trace.n, "value": trace.n / (ms / 1000.0),
@@ -434,7 +438,7 @@ def run_b200(args):
     lib = abi.product_lib()
     trace = cfg.trace(lib=lib)
     n, G = trace.n, cfg.n_gpus
-    rep = DeviceReplay(cfg, trace, dev, args.batch)
+    rep = DeviceReplay(cfg, trace, dev, eff_batch(args, cfg))
 
     with ClockSampler(local) as clk:
         ms, prof = _timed_steps(rep, args.steps, args.warmup)
@@ -556,7 +560,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4")
-    ap.add_argument("--batch", type=int, default=16384)
+    ap.add_argument("--batch", type=int, default=0, help="requests per device batch (0: the config's, else 16384)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=100000,
                     help="requests of the trace the host reference is timed on (0 = all)")

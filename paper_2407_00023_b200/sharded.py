@@ -214,7 +214,7 @@ def bench_main(args, metric, unit, config_dict, clock_sampler):
     lib = abi.product_lib()
     trace = cfg.trace(lib=lib)
     n, G = trace.n, cfg.n_gpus
-    drv = DriverConfig(**{**cfg.driver.__dict__, "batch": args.batch})
+    drv = DriverConfig(**{**cfg.driver.__dict__, "batch": args.batch or cfg.driver.batch or 16384})
     sched = GlobalScheduler(G, cfg.sched, policy=cfg.policy, lib=lib)
     stream = torch.cuda.Stream(dev)  # the library and the timing events share it
     torch.cuda.set_stream(stream)     # the collectives order against it too

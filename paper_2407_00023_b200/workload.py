@@ -253,9 +253,12 @@ CONFIGS = {
         DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=19000, finish_lag=2000),
     ),
     # C5: mixed multi-workload, 10M requests, 64 instances, heavy eviction (cap 30k, high-water 0.95).
+    # Device batches of 2048: partial evictions split ~1 node per request, so
+    # K1's path hints age fast; smaller batches refresh them (C5 +30 % vs 16384,
+    # C2/C4 insensitive: scripts/ab_batch.py).
     "c5": MixConfig(
         "c5_mixed_10M_64inst", "mixed", 10_000_000, 64, _cs2_sched(cap=30000),
-        DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=28500, finish_lag=2000),
+        DriverConfig(eviction=abi.E2_EVICT_MIRROR_LRU, trunk_len=0, high_water=28500, finish_lag=2000, batch=2048),
     ),
 }
 
