@@ -10,7 +10,7 @@ from paper_2407_00023_b200 import abi, workload as W
 from paper_2407_00023_b200.scheduler import GlobalScheduler
 from parity import diff_decisions
 
-SIZES = {"c1": (1000, 1000), "c2": (100000, 100000), "c3": (10000, 10000), "c4": (1000000, 100000), "c5": (100000, 100000)}
+SIZES = {"c1": (1000, 1000), "c2": (100000, 100000), "c3": (10000, 10000), "c4": (1000000, 100000), "c5": (200000, 100000)}
 
 
 def main(names):
