@@ -1,8 +1,8 @@
 #!/bin/bash
-# round 2 evidence: GPU tests, bench (C4 headline) + reference arm, ncu launch list, k_match/k_serial captures on C4
+# round evidence: GPU tests, bench (C4 headline) + reference arm, ncu launch list, K1/top/k_serial captures on C4, configs C1-C3
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-tag=${1:-r2i}
+tag=${1:-evidence}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 timeout 1800 python -m pytest tests -x -q -m gpu --durations=8 > gpurun_out/pytest_$tag.log 2>&1; tail -12 gpurun_out/pytest_$tag.log
 timeout 1500 python bench.py --steps 3 --warmup 3 > gpurun_out/bench_$tag.json 2>gpurun_out/bench_$tag.err; tail -c 1200 gpurun_out/bench_$tag.json; tail -2 gpurun_out/bench_$tag.err
