@@ -12,3 +12,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ma
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_top_build -s 5 -c 1 -o gpurun_out/top_c4_$tag python bench.py --probe --config c4 --probe-n 100000 > gpurun_out/ncu_top_$tag.log 2>&1; tail -1 gpurun_out/ncu_top_$tag.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_serial -s 5 -c 1 -o gpurun_out/serial_c4_$tag python bench.py --probe --config c4 --probe-n 100000 > gpurun_out/ncu_serial_$tag.log 2>&1; tail -1 gpurun_out/ncu_serial_$tag.log
 timeout 600 python scripts/configs_report.py c1 c2 c3 > gpurun_out/configs_$tag.jsonl 2>&1; cut -c1-600 gpurun_out/configs_$tag.jsonl
+timeout 1500 python scripts/configs_report.py c5 2>&1 | cut -c1-600 >> gpurun_out/configs_$tag.jsonl; tail -1 gpurun_out/configs_$tag.jsonl
