@@ -731,7 +731,21 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
       PHASE_MARK1(23);  // waiting
       if (have) replay_out(psb, a, pli, pdec);
       PHASE_MARK1(22);  // decision record
-      while (pp->fix_ready != ci + 1 && !*(volatile i32*)&pp->stop) wait_pause();
+      // wait for warp 0's path update of ci; meanwhile apply its deferred
+      // re-keying of a split suffix (lane 0 reads the flags: warp-uniform)
+      for (;;) {
+        u32 st = 0;
+        if (lane0())
+          st = (pp->fix_ready == ci + 1 ? 1u : 0u) | (*(volatile i32*)&pp->stop ? 2u : 0u) |
+               (g_rkd.pending ? 4u : 0u);
+        st = shfl(st, 0);
+        if (st & 4u) {
+          rekey_deferred();
+          continue;
+        }
+        if (st & 3u) break;
+        wait_pause();
+      }
       acquire_after_poll();
       PHASE_MARK1(31);  // waiting for warp 0's path update
       bool go = pp->fix_ready == ci + 1 && !*(volatile i32*)&pp->stop;
@@ -748,6 +762,7 @@ E2_D void replay_pipe(Scr* s2, const SerialArgs& a, Pipe* pp) {
         go = pp->commit_done == ci + 1;
       }
       if (!go || !pp->c_ok || *(volatile i32*)&HOT.err) {
+        if (shfl((u32)g_rkd.pending, 0)) rekey_deferred();  // keep the LRU index consistent
         if (g_ctd.pending) {  // the failing request's leaf: keep the table consistent
           child_insert(g_ctd.parent, g_ctd.tok, g_ctd.child);
           if (lane0()) g_ctd.pending = 0;

@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
   }
   if (threadIdx.x == 0) {
     g_ctd.pending = 0;
+    g_rkd.pending = 0;
     g_defer_ct = (a.kind == 0 && blockDim.x >= 64) ? 1u : 0u;  // the pipelined replay only
     g_probed = 0;
     g_pf_cur = -1;

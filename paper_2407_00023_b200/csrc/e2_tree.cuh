@@ -84,6 +84,17 @@ struct CtDefer {
   u32 pending;
 };
 __shared__ CtDefer g_ctd;
+// Deferred LRU re-keying of a split's suffix (pipelined replay): the suffix
+// is off the committing request's path, so its leaf keys on the instances
+// caching it can take the new id on the eviction warp, which does it while
+// it waits for warp 0's path update (before its LRU fixes and evictions).
+struct RekeyDefer {
+  u64 mask;  // instances where the suffix is an LRU leaf
+  u64 old_id, new_id;
+  u32 slot;
+  volatile u32 pending;
+};
+__shared__ RekeyDefer g_rkd;
 __shared__ u32 g_defer_ct;  // warp 0 of the pipelined replay defers
 __shared__ u32 g_probed;    // a walk probed the child table
 E2_D void note_probe() {
@@ -949,6 +960,28 @@ E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
   wsync();
   if (!rekey) return q;
   // LRU: the suffix inherits the leaf role under its new id.
+#if E2_WARP
+  if (g_defer_ct && threadIdx.x < 32 && !g_rkd.pending) {
+    if (lane0()) {
+      const NodeRec* r = nget(s);
+      u64 lm = 0;
+      for (u64 m = hs.cmask; m; m &= m - 1) {
+        const int g = ffs64(m);
+        if (rccc(r, G)[g] == 0) lm |= 1ull << g;
+      }
+      if (lm) {
+        g_rkd.mask = lm;
+        g_rkd.old_id = hs.id;
+        g_rkd.new_id = new_id;
+        g_rkd.slot = s;
+        __threadfence_block();
+        g_rkd.pending = 1;
+      }
+    }
+    wsync();
+    return q;
+  }
+#endif
   u64 m = hs.cmask;
   while (m) {
     const int g = ffs64(m);
@@ -958,6 +991,24 @@ E2_DNI u32 split_node(u32 s, u32 k, bool rekey = true) {
   }
   return q;
 }
+
+#if E2_WARP
+// The eviction warp: apply a deferred re-keying (see RekeyDefer).
+// Warp-uniform caller: g_rkd.pending was seen set (by lane 0).
+E2_D void rekey_deferred() {
+  __threadfence_block();
+  const int G = DEV.cfg.G;
+  const u32 s = g_rkd.slot;
+  for (u64 m = g_rkd.mask; m; m &= m - 1) {
+    const int g = ffs64(m);
+    const NodeRec* r = nget(s);
+    lru_rekey(g, dbits(rla(r)[g]), g_rkd.old_id, g_rkd.new_id, s);
+  }
+  wsync();
+  if (lane0()) g_rkd.pending = 0;
+  wsync();
+}
+#endif
 
 // warp-wide: new leaf under parent with edge [off, off+len).
 E2_DNI u32 new_leaf(u32 parent, i64 off, u32 len, u32 depth) {
