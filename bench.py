@@ -171,7 +171,7 @@ def run_reference_arm(args):
         return 0  # rank 0 alone times the host reference
     cfg = workload.CONFIGS[args.config]
     lib = _ref_lib()  # the only native library this process maps
-    n_sample = min(args.ref_sample, cfg.n_requests) if args.ref_sample > 0 else cfg.n_requests
+    n_sample = ref_sample_size(args, cfg)
     trace = cfg.trace(lib=lib, n_requests=n_sample)
     drv = cfg.driver
     times = []
@@ -209,6 +209,17 @@ def run_reference_arm(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def ref_sample_size(args, cfg) -> int:
+    """Requests of the trace one reference step replays.  Default: the whole
+    config when the run has at most 8 steps in all (C4: ~22 s per step), else
+    a 300k-request prefix so the arm stays within a few minutes."""
+    if args.ref_sample > 0:
+        return min(args.ref_sample, cfg.n_requests)
+    if args.ref_sample == 0 or args.steps + args.warmup <= 8:
+        return cfg.n_requests
+    return min(300000, cfg.n_requests)
 
 
 def eff_batch(args, cfg) -> int:
@@ -359,7 +370,7 @@ class DeviceReplay:
         h_dec = torch.empty(self.n * DECISION_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
         h_cost = torch.empty(self.n * (self.G + 1) * COST_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
         ms = []
-        for k in range(runs + 1):
+        for k in range(runs):  # the device path is warm (timed steps ran first)
             lib.e2_reset(h)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -370,8 +381,7 @@ class DeviceReplay:
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             assert rc == 0 and self.done.value == self.n, lib.e2_last_error(h)
-            if k > 0:
-                ms.append(1000 * dt)
+            ms.append(1000 * dt)
         dec = np.frombuffer(h_dec.numpy().tobytes(), dtype=DECISION_DTYPE)
         h2d = int(tr.nbytes)
         d2h = int(self.n * DECISION_DTYPE.itemsize + self.n * (self.G + 1) * COST_DTYPE.itemsize)
@@ -443,7 +453,7 @@ def run_b200(args):
     with ClockSampler(local) as clk:
         ms, prof = _timed_steps(rep, args.steps, args.warmup)
     dec = rep.decisions()
-    e2e_ms, dec_e2e, h2d, d2h = rep.e2e(max(1, min(args.steps, 3)))
+    e2e_ms, dec_e2e, h2d, d2h = rep.e2e(max(1, min(args.steps, 2)))
     assert np.array_equal(dec, dec_e2e), "device-resident and host-buffer replays disagree"
     nodes = rep.sched.node_count()
     rep.close()
@@ -481,7 +491,7 @@ def run_b200(args):
         return t["dram_bytes_per_launch"] / t["requests_per_launch"] * per_launch_requests
 
     cores = _host_cores()
-    ref_n = min(args.ref_sample, n) if args.ref_sample > 0 else n
+    ref_n = min(300000, n)  # cpu_baseline: a bounded sample (~13 s of host work on C4)
     cpu = None
     if os.path.exists(abi.REF_SO):
         rlib = _ref_lib()
@@ -562,8 +572,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--batch", type=int, default=0, help="requests per device batch (0: the config's, else 16384)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=100000,
-                    help="requests of the trace the host reference is timed on (0 = all)")
+    ap.add_argument("--ref-sample", type=int, default=-1,
+                    help="requests the host reference is timed on per step (0: all; default: all when steps+warmup <= 8, else 300k)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-traffic", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)  # gloo: dev check on one GPU
