@@ -204,6 +204,19 @@ int e2_debug_dump(e2_handle* h, double now, char* buf, size_t cap, size_t* neede
 /* Window contents after pruning at now (snapshot(), global_scheduler.cpp:375-394). */
 int e2_window_sizes(e2_handle* h, int32_t gpu, double now, int64_t* n_scheduled,
                     int64_t* n_completed, int64_t* inflight_cached, int64_t* inflight_prompt);
+/* snapshot(now).gpus[gpu].scheduled / .completed — global_scheduler.cpp:384-389,
+ * LoadWindow::snapshot_scheduled/completed (cost_model.cpp:55-63): the
+ * entries after pruning at now, oldest first, sized by e2_window_sizes.
+ * Any pointer may be NULL. */
+int e2_window_entries(e2_handle* h, int32_t gpu, double now, double* sched_t, int64_t* sched_missed,
+                      int64_t* sched_est, double* comp_t, int64_t* comp_out);
+/* snapshot(now).nodes[i].hits — export_nodes (prefix_tree.cpp:436-448) hit
+ * stamps in e2_export's node order, gpu-minor, each list oldest first; list
+ * (i, g) holds e2_export's hits[i*G+g] stamps.  Only in-window stamps
+ * (t >= now - history_window_ms): what every read of the reference sees
+ * after its lazy prune (prefix_tree.cpp:37-43); the reference's raw deques
+ * may still hold older ones.  *n_stamps = total; stamps may be NULL. */
+int e2_export_hit_stamps(e2_handle* h, double now, double* stamps, int64_t cap, int64_t* n_stamps);
 
 /* ---------------------------------------------------------------------------
  * Batched trace driver.  The reference's own throughput loop

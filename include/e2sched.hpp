@@ -8,8 +8,10 @@
 // linking libe2sched.so.  The reference's types come from its own headers.
 //
 // Not provided: mirror() (the tree lives in HBM; use cached_tokens(),
-// debug_dump() or match() instead — a host PrefixTree materialisation would
-// be an export, a slow path) and snapshot() (use e2_export / e2_window_sizes).
+// debug_dump(), snapshot() or match() instead — a host PrefixTree
+// materialisation would be an export, a slow path).  snapshot() is provided;
+// its NodeSnapshot::hits hold the in-window stamps (t >= now - H), what
+// every read of the reference sees after its lazy prune.
 #pragma once
 
 #include <map>
@@ -25,7 +27,7 @@ namespace b200 {
 class GlobalScheduler {
  public:
   GlobalScheduler(int n_gpus, const SchedulerConfig& config, const TimeModel& model, const GlobalPolicy& policy)
-      : n_(n_gpus), config_(config), model_(model) {
+      : n_(n_gpus), config_(config), model_(model), policy_(policy) {
     e2_sched_cfg c{config.history_window_ms, config.th_bal,        config.imbal_ratio,
                    config.priority_groups,   config.kv_capacity_tokens, config.default_output_len};
     e2_time_model m{model.prefill_base_ms, model.prefill_per_token_ms, model.decode_per_token_ms,
@@ -117,6 +119,55 @@ class GlobalScheduler {
     o.tree_reads = s.tree_reads;
     return o;
   }
+  // snapshot(now) — global_scheduler.cpp:375-394
+  ClusterSnapshot snapshot(SimTime now) {
+    ClusterSnapshot snap;
+    snap.now = now;
+    snap.n_gpus = n_;
+    snap.config = config_;
+    snap.model = model_;
+    snap.policy = policy_;
+    int64_t nn = 0, nt = 0, ns = 0;
+    check(e2_export_size(h_, &nn, &nt), h_);
+    std::vector<e2_node> nodes(nn);
+    std::vector<int32_t> tok(nt);
+    std::vector<double> la(nn * n_);
+    std::vector<int64_t> hits(nn * n_);
+    check(e2_export(h_, now, nodes.data(), tok.data(), la.data(), hits.data()), h_);
+    check(e2_export_hit_stamps(h_, now, nullptr, 0, &ns), h_);
+    std::vector<double> st(ns);
+    check(e2_export_hit_stamps(h_, now, st.data(), ns, &ns), h_);
+    int64_t k = 0;
+    for (int64_t i = 0; i < nn; ++i) {
+      PrefixTree::NodeSnapshot o;
+      o.id = nodes[i].id;
+      o.parent_id = nodes[i].parent_id;
+      o.edge.assign(tok.begin() + nodes[i].edge_off, tok.begin() + nodes[i].edge_off + nodes[i].edge_len);
+      for (int g = 0; g < n_; ++g) {
+        if ((nodes[i].caching_mask >> g) & 1ull) o.caching_gpus.push_back(g);
+        if ((nodes[i].last_access_mask >> g) & 1ull) o.last_access[g] = la[i * n_ + g];
+        const int64_t c = hits[i * n_ + g];
+        if (c > 0) o.hits[g].assign(st.begin() + k, st.begin() + k + c);
+        k += c;
+      }
+      o.pin_count = (int)nodes[i].pin_count;
+      snap.nodes.push_back(std::move(o));
+    }
+    for (int g = 0; g < n_; ++g) {
+      ClusterSnapshot::GpuSnap gs;
+      gs.id = g;
+      int64_t nsch = 0, ncomp = 0;
+      check(e2_window_sizes(h_, g, now, &nsch, &ncomp, &gs.inflight_cached, &gs.inflight_prompt), h_);
+      std::vector<double> t(nsch), ct(ncomp);
+      std::vector<int64_t> m(nsch), e(nsch), co(ncomp);
+      check(e2_window_entries(h_, g, now, t.data(), m.data(), e.data(), ct.data(), co.data()), h_);
+      for (int64_t i = 0; i < nsch; ++i) gs.scheduled.push_back({t[i], m[i], e[i]});
+      for (int64_t i = 0; i < ncomp; ++i) gs.completed.push_back({ct[i], co[i]});
+      snap.gpus.push_back(std::move(gs));
+    }
+    snap.redirects = redirects();
+    return snap;
+  }
   int n_gpus() const { return n_; }
   const SchedulerConfig& config() const { return config_; }
   const TimeModel& model() const { return model_; }
@@ -164,6 +215,7 @@ class GlobalScheduler {
   int n_;
   SchedulerConfig config_;
   TimeModel model_;
+  GlobalPolicy policy_;
   e2_handle* h_ = nullptr;
   std::vector<e2_cost> costs_;
   std::vector<double> ratios_;

@@ -377,6 +377,45 @@ int e2_export(e2_handle* h, double now, e2_node* nodes, int32_t* tokens, double*
   });
 }
 
+// Both from the reference's own snapshot(now) (global_scheduler.cpp:375-394).
+int e2_window_entries(e2_handle* h, int32_t gpu, double now, double* sched_t, int64_t* sched_missed,
+                      int64_t* sched_est, double* comp_t, int64_t* comp_out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    ClusterSnapshot snap = h->s->snapshot(now);
+    const auto& g = snap.gpus[gpu];
+    for (size_t i = 0; i < g.scheduled.size(); ++i) {
+      if (sched_t) sched_t[i] = g.scheduled[i].t;
+      if (sched_missed) sched_missed[i] = g.scheduled[i].missed;
+      if (sched_est) sched_est[i] = g.scheduled[i].est_output;
+    }
+    for (size_t i = 0; i < g.completed.size(); ++i) {
+      if (comp_t) comp_t[i] = g.completed[i].t;
+      if (comp_out) comp_out[i] = g.completed[i].output;
+    }
+  });
+}
+
+int e2_export_hit_stamps(e2_handle* h, double now, double* stamps, int64_t cap, int64_t* n_stamps) {
+  return guard(h, [&] {
+    ClusterSnapshot snap = h->s->snapshot(now);
+    const double horizon = h->s->config().history_window_ms;
+    int64_t k = 0;
+    for (const auto& s : snap.nodes)
+      for (int g = 0; g < h->n; ++g) {
+        auto it = s.hits.find(g);
+        if (it == s.hits.end()) continue;
+        for (double t : it->second) {
+          if (!(t >= now - horizon)) continue;
+          if (stamps && k < cap) stamps[k] = t;
+          k++;
+        }
+      }
+    if (n_stamps) *n_stamps = k;
+    if (stamps && k > cap) throw std::invalid_argument("stamps buffer too small");
+  });
+}
+
 int e2_debug_dump(e2_handle* h, double now, char* buf, size_t cap, size_t* needed) {
   return guard(h, [&] {
     std::string s = h->s->mirror().debug_dump(now, h->s->config().history_window_ms);

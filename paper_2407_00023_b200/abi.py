@@ -263,6 +263,12 @@ _CORPUS_SIGS = {
 #: checkers have no sharded or streamed replay.
 PRODUCT_ONLY = tuple(_PRODUCT_SIGS)
 _PRODUCT_SIGS.update(_CORPUS_SIGS)
+#: snapshot() pieces beyond export/window sizes (product and reference shim;
+#: the plain-C oracle has no snapshot).
+_PRODUCT_SIGS.update({
+    "e2_window_entries": (ctypes.c_int, [_h, _i32, _f64, _vp, _vp, _vp, _vp, _vp]),
+    "e2_export_hit_stamps": (ctypes.c_int, [_h, _f64, _vp, _i64, P(_i64)]),
+})
 
 #: Every symbol include/e2sched.h declares (checked by the CPU test suite).
 DECLARED_SYMBOLS = tuple(_SIGS) + tuple(_PRODUCT_SIGS)

@@ -2139,6 +2139,22 @@ int e2_window_sizes(e2_handle* h, int32_t gpu, double now, int64_t* n_scheduled,
 namespace {
 void expire_all(e2_handle* h, double now) { run_simple(h, OP_EXPIRE_ALL, 0, 0, now); }
 
+// Ring positions [head, tail) of instance g's window ring (T = WinEnt or
+// CompEnt), oldest first.
+extern "C++" template <typename T>
+std::vector<T> pull_ring(e2_handle* h, const T* ring, int g, u64 head, u64 tail) {
+  std::vector<T> out(tail - head);
+  const u64 cap = h->d.wcap;
+  for (u64 i = head; i < tail;) {
+    const u64 at = i & (cap - 1);
+    const u64 run = std::min<u64>(tail - i, cap - at);
+    d2h(out.data() + (i - head), ring + (u64)g * cap + at, run * sizeof(T), h->stream);
+    i += run;
+  }
+  ssync(h->stream);
+  return out;
+}
+
 void dfs_order(const HostTree& t, std::vector<std::pair<u32, int>>& order) {
   std::vector<std::pair<u32, int>> st{{kRoot, 0}};
   while (!st.empty()) {
@@ -2192,6 +2208,70 @@ int e2_export(e2_handle* h, double now, e2_node* nodes, int32_t* tokens, double*
         if (hits) hits[i * G + g] = t.hits[(u64)x * G + g];
       }
     }
+  });
+}
+
+// snapshot(now)'s windows (global_scheduler.cpp:384-389): after pruning at
+// now, the scheduled and completed entries, oldest first.
+int e2_window_entries(e2_handle* h, int32_t gpu, double now, double* sched_t, int64_t* sched_missed,
+                      int64_t* sched_est, double* comp_t, int64_t* comp_out) {
+  if (bad_gpu(h, gpu)) return E2_ERR_ARG;
+  return guard(h, [&] {
+    OpDesc op;
+    memset(&op, 0, sizeof(op));
+    op.kind = OP_WINDOW;  // prunes gpu's window at now
+    op.gpu = gpu;
+    op.now = now;
+    run_api(h, op, nullptr, 0, false);
+    const auto ws = pull_ring(h, h->d.win, gpu, h->hot.ws_head[gpu], h->hot.ws_tail[gpu]);
+    for (size_t i = 0; i < ws.size(); ++i) {
+      if (sched_t) sched_t[i] = ws[i].t;
+      if (sched_missed) sched_missed[i] = ws[i].missed;
+      if (sched_est) sched_est[i] = ws[i].est;
+    }
+    const auto wc = pull_ring(h, h->d.comp, gpu, h->hot.wc_head[gpu], h->hot.wc_tail[gpu]);
+    for (size_t i = 0; i < wc.size(); ++i) {
+      if (comp_t) comp_t[i] = wc[i].t;
+      if (comp_out) comp_out[i] = wc[i].out;
+    }
+  });
+}
+
+// NodeSnapshot::hits (prefix_tree.cpp:436-448), in-window stamps only.  The
+// counter identity (DESIGN §3 fact 3) says node n's hits on g are the
+// in-window scheduled entries of g whose prompt passes through n; that
+// prompt's path is the parent chain of the entry's tail slot (splits insert
+// above it, the slot keeps the suffix).  So each entry's time is stamped on
+// its chain, entries in window order; the per-node counts must equal the
+// device's counters (checked).
+int e2_export_hit_stamps(e2_handle* h, double now, double* stamps, int64_t cap, int64_t* n_stamps) {
+  return guard(h, [&] {
+    expire_all(h, now);
+    HostTree t;
+    pull_tree(h, t);
+    const int G = h->G;
+    const u64 n = t.hdr.size();
+    std::vector<std::vector<double>> st(n * (u64)G);
+    for (int g = 0; g < G; ++g) {
+      const auto ws = pull_ring(h, h->d.win, g, h->hot.ws_head[g], h->hot.ws_tail[g]);
+      for (const WinEnt& e : ws)
+        for (u32 x = e.slot; x != kRoot && x != kNil && x < n; x = t.hdr[x].parent) st[(u64)x * G + g].push_back(e.t);
+    }
+    std::vector<std::pair<u32, int>> order;
+    dfs_order(t, order);
+    i64 k = 0;
+    for (auto& [x, dep] : order)
+      for (int g = 0; g < G; ++g) {
+        const auto& v = st[(u64)x * G + g];
+        if ((i64)v.size() != (i64)t.hits[(u64)x * G + g])
+          throw Fail(E2_ERR_SIM, "hit stamps disagree with the hit counters");
+        for (double s : v) {
+          if (stamps && k < cap) stamps[k] = s;
+          k++;
+        }
+      }
+    if (n_stamps) *n_stamps = k;
+    if (stamps && k > cap) throw Fail(E2_ERR_ARG, "stamps buffer too small");
   });
 }
 

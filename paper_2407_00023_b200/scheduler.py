@@ -166,6 +166,35 @@ class NodeExport:  # PrefixTree::NodeSnapshot (prefix_tree.hpp:186-194), hits as
     pin_count: int
 
 
+@dataclasses.dataclass
+class NodeSnapshot:  # PrefixTree::NodeSnapshot (prefix_tree.hpp:170-178); hits: in-window stamps
+    id: int
+    parent_id: int
+    edge: tuple
+    caching_gpus: tuple
+    hits: Dict[int, List[float]]
+    last_access: Dict[int, float]
+    pin_count: int
+
+
+@dataclasses.dataclass
+class GpuSnap:  # ClusterSnapshot::GpuSnap (global_scheduler.hpp:74-80)
+    id: int
+    scheduled: List[tuple]  # LoadWindow::Scheduled (t, missed, est_output)
+    completed: List[tuple]  # LoadWindow::Completed (t, output)
+    inflight_cached: int
+    inflight_prompt: int
+
+
+@dataclasses.dataclass
+class ClusterSnapshot:  # global_scheduler.hpp:67-83 (config/model/policy: the scheduler's own)
+    now: float
+    n_gpus: int
+    nodes: List[NodeSnapshot]
+    gpus: List[GpuSnap]
+    redirects: Dict[int, int]
+
+
 def _tokens(seq) -> np.ndarray:
     a = np.ascontiguousarray(np.asarray(seq, dtype=np.int32))
     return a
@@ -375,6 +404,38 @@ class GlobalScheduler:
                 )
             )
         return out
+
+    def snapshot(self, now: float) -> ClusterSnapshot:
+        """snapshot(now) (global_scheduler.cpp:375-394).  Node hits hold the
+        in-window stamps (t >= now - H), which is what the reference's reads
+        see after their lazy prune; its raw deques may hold older ones."""
+        gpus = []
+        for g in range(self._n):
+            ns, nc, ic, ip = self.window_sizes(g, now)
+            st, sm, se = np.zeros(ns), np.zeros(ns, dtype=np.int64), np.zeros(ns, dtype=np.int64)
+            ct, co = np.zeros(nc), np.zeros(nc, dtype=np.int64)
+            self._check(self._lib.e2_window_entries(self._h, g, float(now), _ptr(st), _ptr(sm), _ptr(se), _ptr(ct), _ptr(co)))
+            gpus.append(GpuSnap(g, list(zip(st.tolist(), sm.tolist(), se.tolist())), list(zip(ct.tolist(), co.tolist())), ic, ip))
+        nodes, toks, la, hits = self.export_arrays(now)
+        total = ctypes.c_int64()
+        self._check(self._lib.e2_export_hit_stamps(self._h, float(now), None, 0, ctypes.byref(total)))
+        stamps = np.zeros(max(total.value, 1))
+        self._check(self._lib.e2_export_hit_stamps(self._h, float(now), _ptr(stamps), total.value, ctypes.byref(total)))
+        out, k = [], 0
+        for i, n in enumerate(nodes):
+            hm = {}
+            for g in range(self._n):
+                c = int(hits[i, g])
+                if c:
+                    hm[g] = stamps[k : k + c].tolist()
+                    k += c
+            out.append(NodeSnapshot(
+                n.id, n.parent_id, tuple(toks[n.edge_off : n.edge_off + n.edge_len].tolist()),
+                tuple(g for g in range(self._n) if (n.caching_mask >> g) & 1), hm,
+                {g: float(la[i, g]) for g in range(self._n) if (n.last_access_mask >> g) & 1}, n.pin_count))
+        if k != total.value:
+            raise SimError(f"snapshot: {total.value} hit stamps for {k} windowed hits")
+        return ClusterSnapshot(float(now), self._n, out, gpus, self.redirects())
 
     def debug_dump(self, now: float) -> str:
         need = ctypes.c_size_t()

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <deque>
 
 #include "e2sched.hpp"
@@ -25,6 +26,40 @@ static bool same(const Decision& a, const Decision& b) {
         x.eviction_ms != y.eviction_ms || x.prefill_ms != y.prefill_ms ||
         x.eviction_infeasible != y.eviction_infeasible)
       return false;
+  }
+  return true;
+}
+
+// snapshot(now) of both sides (global_scheduler.cpp:375-394); the
+// reference's raw hit deques are read through the window like any of its
+// reads (prefix_tree.cpp:37-43).
+static bool same_snapshot(ClusterSnapshot a, const ClusterSnapshot& b, SimTime horizon) {
+  if (a.now != b.now || a.n_gpus != b.n_gpus || a.redirects != b.redirects || a.nodes.size() != b.nodes.size() ||
+      a.gpus.size() != b.gpus.size())
+    return false;
+  for (size_t i = 0; i < a.nodes.size(); ++i) {
+    auto& x = a.nodes[i];
+    const auto& y = b.nodes[i];
+    for (auto it = x.hits.begin(); it != x.hits.end();) {
+      auto& v = it->second;
+      v.erase(v.begin(), std::find_if(v.begin(), v.end(), [&](SimTime t) { return !(t < a.now - horizon); }));
+      it = v.empty() ? x.hits.erase(it) : std::next(it);
+    }
+    if (x.id != y.id || x.parent_id != y.parent_id || x.edge != y.edge || x.caching_gpus != y.caching_gpus ||
+        x.hits != y.hits || x.last_access != y.last_access || x.pin_count != y.pin_count)
+      return false;
+  }
+  for (size_t g = 0; g < a.gpus.size(); ++g) {
+    const auto &x = a.gpus[g], &y = b.gpus[g];
+    if (x.id != y.id || x.inflight_cached != y.inflight_cached || x.inflight_prompt != y.inflight_prompt ||
+        x.scheduled.size() != y.scheduled.size() || x.completed.size() != y.completed.size())
+      return false;
+    for (size_t i = 0; i < x.scheduled.size(); ++i)
+      if (x.scheduled[i].t != y.scheduled[i].t || x.scheduled[i].missed != y.scheduled[i].missed ||
+          x.scheduled[i].est_output != y.scheduled[i].est_output)
+        return false;
+    for (size_t i = 0; i < x.completed.size(); ++i)
+      if (x.completed[i].t != y.completed[i].t || x.completed[i].output != y.completed[i].output) return false;
   }
   return true;
 }
@@ -89,6 +124,10 @@ int main(int argc, char** argv) {
     t2 = clk::now();
     t_ref += std::chrono::duration<double>(t1 - t0).count();
     t_dut += std::chrono::duration<double>(t2 - t1).count();
+    if ((i + 1) % 1000 == 0 && !same_snapshot(ref.snapshot(now), dut.snapshot(now), cfg.history_window_ms)) {
+      std::printf("snapshot MISMATCH after request %zu\n", i);
+      return 1;
+    }
   }
   const GlobalStats sa = ref.stats(), sb = dut.stats();
   if (sa.exploit != sb.exploit || sa.explore != sb.explore || sa.redirected != sb.redirected ||

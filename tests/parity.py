@@ -63,6 +63,23 @@ def export_diff(sa: GlobalScheduler, sb: GlobalScheduler, now: float):
     return None
 
 
+def snapshot_diff(sa: GlobalScheduler, sb: GlobalScheduler, now: float):
+    """Compare snapshot(now) (global_scheduler.cpp:375-394) field by field,
+    doubles as raw bits (== on floats; no NaNs occur).  Message or None."""
+    a, b = sa.snapshot(now), sb.snapshot(now)
+    if (a.now, a.n_gpus, a.redirects) != (b.now, b.n_gpus, b.redirects):
+        return "header/redirects differ"
+    if len(a.nodes) != len(b.nodes):
+        return f"node count {len(a.nodes)} != {len(b.nodes)}"
+    for i, (x, y) in enumerate(zip(a.nodes, b.nodes)):
+        if x != y:
+            return f"node {i}: {x} vs {y}"
+    for x, y in zip(a.gpus, b.gpus):
+        if x != y:
+            return f"gpu {x.id}: {x} vs {y}"
+    return None
+
+
 def assert_same_state(sa, sb, now):
     assert sa.stats() == sb.stats()
     assert sa.node_count() == sb.node_count()

@@ -25,7 +25,7 @@ from paper_2407_00023_b200.scheduler import (
     TimeModel,
 )
 
-from parity import export_diff
+from parity import export_diff, snapshot_diff
 
 
 def _same_decision(a, b):
@@ -73,6 +73,10 @@ def run_case(lib, ref_lib, seed, stats):
                     extra = 1 + rng.randrange(15)
                     prompt += list(range(unique, unique + extra))
                     unique += extra
+            if rng.randrange(4) == 0:  # the reference harness snapshots before each decision (:333)
+                stats["snapshots"] += 1
+                msg = snapshot_diff(A, B, t)
+                assert msg is None, (seed, op, msg)
             req = Request(next_id, prompt, t, 1 + rng.randrange(40))
             errs = []
             outs = []
@@ -139,12 +143,14 @@ def run_case(lib, ref_lib, seed, stats):
     assert A.redirects() == B.redirects()
     msg = export_diff(A, B, t)
     assert msg is None, (seed, msg)
+    msg = snapshot_diff(A, B, t)
+    assert msg is None, (seed, msg)
     A.close()
     B.close()
 
 
 def _fuzz(lib, ref_lib, cases, base):
-    stats = dict(decisions=0, exploit=0, pressure=0, redirected=0, probes=0, infeasible=0)
+    stats = dict(snapshots=0, decisions=0, exploit=0, pressure=0, redirected=0, probes=0, infeasible=0)
     for c in range(cases):
         run_case(lib, ref_lib, base * 1000003 + c, stats)
     # the comparison must not be vacuous (test_scheduler_oracle.cpp:17-21)
