@@ -7,6 +7,7 @@
 // The same file compiled by g++ with -DE2_HOSTSIM (tests/_build only) runs
 // the identical engine on the host with a warp width of 1; that build is a
 // test double for the CPU suite and is never shipped.
+#include <atomic>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -146,11 +147,9 @@ constexpr size_t kScrBytes = (2 * sizeof(Scr) + 127) / 128 * 128;
 // two-warp pipeline of e2_kernels.cuh (warp 1 runs the evictions).
 // Dynamic shared memory: two Scr buffers (the pipeline alternates them per
 // request), then the node-cache arrays (a stub unless E2_SMEM_NODECACHE).
-__global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
-  __shared__ Pipe pipe;
-  extern __shared__ __align__(16) char dyn0[];
-  Scr* ss = (Scr*)dyn0;
-  char* dyn = dyn0 + kScrBytes;
+// Block prologue shared by k_serial and k_session: the hot state into shared
+// memory (warp 0), the node-cache arrays, the pipeline's flags.
+__device__ void serial_prologue(u32 nsets, char* dyn, Scr* ss, Pipe* pipe, bool pipelined) {
   const u32 ne = nsets * kWays;
   if (threadIdx.x < 32) {
     const u64* src = (const u64*)g_dev.hot_g;
@@ -173,28 +172,196 @@ __global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
   if (threadIdx.x == 0) {
     g_ctd.pending = 0;
     g_rkd.pending = 0;
-    g_defer_ct = (a.kind == 0 && blockDim.x >= 64) ? 1u : 0u;  // the pipelined replay only
+    g_defer_ct = pipelined ? 1u : 0u;  // the pipelined replay only
     g_probed = 0;
     g_pf_cur = -1;
     g_pf_stop = 0;
-    pipe.ready = 0;
-    pipe.books_done = 0;
-    pipe.fix_ready = 0;
-    pipe.commit_done = 0;
-    pipe.w1_fixed = 0;
-    pipe.c_ok = 0;
-    pipe.stop = 0;
+    if (pipe) {
+      pipe->ready = 0;
+      pipe->books_done = 0;
+      pipe->fix_ready = 0;
+      pipe->commit_done = 0;
+      pipe->w1_fixed = 0;
+      pipe->c_ok = 0;
+      pipe->stop = 0;
+    }
     ss[0].win_done = ss[1].win_done = 0;
   }
-  __syncthreads();
-  serial_body(ss, a, blockDim.x >= 64 ? &pipe : nullptr);
-  __syncwarp();  // the warps leave their polling loops lane by lane
-  __syncthreads();
+}
+
+__device__ void serial_epilogue() {
   if (threadIdx.x < 32) {
     const u64* src = (const u64*)&g_hot;
     u64* dst = (u64*)g_dev.hot_g;
     for (u32 i = threadIdx.x; i < sizeof(Hot) / 8; i += 32) dst[i] = src[i];
   }
+}
+
+__global__ void __launch_bounds__(128, 1) k_serial(SerialArgs a, u32 nsets) {
+  __shared__ Pipe pipe;
+  extern __shared__ __align__(16) char dyn0[];
+  Scr* ss = (Scr*)dyn0;
+  serial_prologue(nsets, dyn0 + kScrBytes, ss, &pipe, a.kind == 0 && blockDim.x >= 64);
+  __syncthreads();
+  serial_body(ss, a, blockDim.x >= 64 ? &pipe : nullptr);
+  __syncwarp();  // the warps leave their polling loops lane by lane
+  __syncthreads();
+  serial_epilogue();
+}
+
+// ---- per-call session: a persistent one-warp kernel ------------------------
+// The per-call API (e2_schedule, note_*, ...) costs a launch, a hot-state
+// round trip through HBM and a stream synchronisation per call when each op
+// is its own k_serial launch.  A session keeps one warp resident with the hot
+// state in shared memory: the host writes the op (and its prompt tokens) into
+// a pinned, device-mapped command block and bumps `seq`; the warp polls it,
+// copies the tokens into the arena, runs the same api_op, writes ApiOut and
+// the hot state into the mapped result block, fences (system scope) and
+// publishes `seq`.  The warp exits on a stop command, on an error, or after
+// `idle_ns` without a command (so a device-wide synchronisation elsewhere
+// never waits on it for long); the host restarts it on the next op.
+struct SessCmd {
+  volatile unsigned long long seq;
+  i32 stop;
+  i32 need_match;
+  i64 ntok;
+  OpDesc op;
+  // prompt tokens follow at kSessTok
+};
+constexpr size_t kSessTok = (sizeof(SessCmd) + 127) / 128 * 128;
+constexpr u32 kSessHdrWords = sizeof(SessCmd) / 8;
+static_assert(sizeof(SessCmd) % 8 == 0 && kSessHdrWords <= 32, "one word per lane");
+struct SessRes {
+  volatile unsigned long long seq;  // last command completed
+  u64 pad[15];
+  ApiOut api;
+  Hot hot;
+};
+
+__shared__ Hot g_hot_pub;  // k_session: the hot state as last published to the host
+constexpr u32 kSessFirst = 4096;  // token bytes read beside the header
+
+__device__ __forceinline__ u64 gtimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(32, 1) k_session(SessCmd* cmd, SessRes* res, unsigned long long next, u32* hint,
+                                                   int hstride, u32 nsets, u64 idle_ns) {
+  extern __shared__ __align__(16) char dyn0[];
+  Scr* ss = (Scr*)dyn0;
+  serial_prologue(nsets, dyn0 + kScrBytes, ss, nullptr, false);
+  __syncwarp();
+  for (u32 i = lane(); i < sizeof(Hot) / 8; i += 32) ((u64*)&g_hot_pub)[i] = ((const u64*)&g_hot)[i];
+  u64 tsum[4] = {res->pad[0], res->pad[1], res->pad[2], res->pad[3]};
+  __syncwarp();
+  u64 t_idle = gtimer();
+  for (;;) {
+    u32 got = 0;
+    if (lane0()) {
+      for (;;) {
+        if (cmd->seq == next) {
+          got = 1;
+          break;
+        }
+        if (gtimer() - t_idle > idle_ns) break;
+        __nanosleep(100);
+      }
+    }
+    got = shfl(got, 0);
+    if (!got) break;
+    const u64 t0 = gtimer();
+    // no acquire fence: the reads below issue after the poll returned the new
+    // seq, and the host made the command visible before the seq (x86 TSO +
+    // its release fence)
+    asm volatile("" ::: "memory");
+    // one wave over the link: lane i reads header word i and the first 4 KB
+    // of tokens are read speculatively beside it (the block always has room).
+    // (A TMA bulk copy from the mapped host block never completes.)
+    __shared__ u64 hdr[kSessHdrWords];
+    const int4* q = (const int4*)((const char*)cmd + kSessTok);
+    int4 v[8];
+    u64 hw = 0;
+    if (lane() < (int)kSessHdrWords) hw = ((const volatile u64*)cmd)[lane()];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
+                   : "l"(q + k * 32 + lane()));
+    if (lane() < (int)kSessHdrWords) hdr[lane()] = hw;
+    __syncwarp();
+    const SessCmd* c = (const SessCmd*)hdr;
+    if (c->stop) break;
+    const OpDesc op = c->op;
+    const i64 ntok = c->ntok;
+    const bool need_match = c->need_match != 0;
+    i32* arena = (i32*)g_dev.tok + op.off;
+    const i64 nq = (ntok + 3) / 4;  // whole quads: the arena has tail slack
+    for (i64 b = 0;; b += 8 * 32) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const i64 j = b + k * 32 + lane();
+        if (j < nq) {
+          arena[4 * j] = v[k].x;
+          if (4 * j + 1 < ntok) arena[4 * j + 1] = v[k].y;
+          if (4 * j + 2 < ntok) arena[4 * j + 2] = v[k].z;
+          if (4 * j + 3 < ntok) arena[4 * j + 3] = v[k].w;
+        }
+      }
+      if (b + 8 * 32 >= nq) break;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const i64 j = b + 8 * 32 + k * 32 + lane();
+        if (j < nq)
+          asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
+                       : "l"(q + j));
+      }
+    }
+    __syncwarp();
+    const u64 t1 = gtimer();
+    if (lane0()) HOT.done = 0;
+    wsync();
+    api_op(ss, op, need_match ? hint : nullptr, hstride, &res->api, nullptr);
+    const u64 t2 = gtimer();
+    if (lane0()) HOT.done = HOT.err ? 0 : 1;
+    wsync();
+    nflush();
+    {
+      // only the words that changed since the last publish (the host keeps
+      // the whole block current)
+      const u64* src = (const u64*)&g_hot;
+      u64* sh = (u64*)&g_hot_pub;
+      volatile u64* dst = (volatile u64*)&res->hot;
+      for (u32 i = lane(); i < sizeof(Hot) / 8; i += 32) {
+        const u64 x = src[i];
+        if (x != sh[i]) {
+          sh[i] = x;
+          dst[i] = x;
+        }
+      }
+    }
+    if (lane0()) {
+      const u64 t3 = gtimer();
+      tsum[0] += t1 - t0;  // command header + tokens
+      tsum[1] += t2 - t1;  // the op
+      tsum[2] += t3 - t2;  // hot state out
+      tsum[3] += 1;
+      for (int k = 0; k < 4; ++k) res->pad[k] = tsum[k];
+    }
+    __threadfence_system();
+    __syncwarp();
+    if (lane0()) res->seq = next;
+    ++next;
+    const bool err = HOT.err != 0;
+    wsync();
+    if (err) break;  // the host stops the session and handles the error on the launch path
+    t_idle = gtimer();
+  }
+  __syncwarp();
+  serial_epilogue();
+  __threadfence_system();
 }
 
 // The staged top image for the next K1 launch (one block): the distinct
@@ -761,6 +928,23 @@ struct e2_handle {
   i64 *cb_ids = nullptr, *cb_out = nullptr;  // combined [carry | chunk] arrays
   double* cb_arr = nullptr;
   i64 cb_cap = 0;
+  // per-call session (k_session): a resident warp fed through pinned,
+  // device-mapped command/result blocks
+  bool sess_on = false;
+  bool no_session = false;  // E2_NO_SESSION=1: every per-call op is its own launch
+  Stream sess_stream = 0;
+  void* sess_cmd = nullptr;  // SessCmd + tokens (pinned, mapped)
+  void* sess_res = nullptr;  // SessRes (pinned, mapped)
+  i64 sess_tok_cap = 0;
+  unsigned long long sess_next = 1;  // the next command number
+  u64 sess_idle_ns = 2000000;
+  std::vector<i32> sess_last;  // tokens of the last committed op sent through the session
+  i64 sess_last_off = 0;
+  bool sess_last_ok = false;
+  i64 sess_ops = 0, sess_starts = 0, sess_relaunch = 0, sess_stops = 0;
+  i64 sess_why[5] = {0, 0, 0, 0, 0};
+  // reserve_* dry run: report (dry_hit) instead of growing
+  bool dry = false, dry_hit = false;
   // profiling
   bool prof = false;
   e2_profile acc;
@@ -846,7 +1030,9 @@ void push_hot(e2_handle* h) {
   h->dev_hot = h->hot;
   h->dev_hot_valid = true;
 }
+bool session_active(const e2_handle* h);
 void pull_hot(e2_handle* h) {
+  if (session_active(h)) return;  // h->hot is the session's last published state
   d2h(&h->hot, h->d.hot_g, sizeof(Hot), h->stream);
   ssync(h->stream);
   h->dev_hot = h->hot;
@@ -902,6 +1088,10 @@ void host_rehash_ct(e2_handle* h, u64 new_cap) {
 void reserve_nodes(e2_handle* h, u64 need) {
   Dev& d = h->d;
   if (need <= d.node_cap && d.rec) return;
+  if (h->dry) {
+    h->dry_hit = true;
+    return;
+  }
   const int G = h->G;
   u64 cap = std::max<u64>(need, (u64)d.node_cap * 2);
   cap = std::max<u64>(cap, 1024);
@@ -978,6 +1168,10 @@ void reserve_window(e2_handle* h, u64 entries) {
   Dev& d = h->d;
   const u64 cap = pow2_at_least(std::max<u64>(entries, 1024));
   if (cap <= d.wcap) return;
+  if (h->dry) {
+    h->dry_hit = true;
+    return;
+  }
   // scheduled entries stay until their hit stamps are undone (ws_done)
   ring_regrow(h, d.win, d.wcap, cap, h->hot.ws_done, h->hot.ws_tail);
   ring_regrow(h, d.comp, d.wcap, cap, h->hot.wc_head, h->hot.wc_tail);
@@ -990,6 +1184,10 @@ void reserve_window(e2_handle* h, u64 entries) {
 constexpr u64 kPlogMin = 1ull << 16, kPlogMax = 1ull << 21;
 void reserve_plog(e2_handle* h) {
   Dev& d = h->d;
+  if (!d.plog && h->dry) {
+    h->dry_hit = true;
+    return;
+  }
   if (!d.plog) {
     d.pcap = kPlogMin;
     d.plog = talloc<u32>(d.pcap * (u64)h->G);
@@ -998,6 +1196,10 @@ void reserve_plog(e2_handle* h) {
   u64 live = 0;
   for (int g = 0; g < h->G; ++g) live = std::max<u64>(live, h->hot.pl_tail[g] - h->hot.pl_head[g]);
   if (live * 2 <= d.pcap || d.pcap >= kPlogMax) return;
+  if (h->dry) {
+    h->dry_hit = true;
+    return;
+  }
   const u64 cap = std::min<u64>(d.pcap * 4, kPlogMax);
   ring_regrow(h, d.plog, d.pcap, cap, h->hot.pl_head, h->hot.pl_tail);
   d.pcap = cap;
@@ -1007,6 +1209,10 @@ void reserve_fifo(e2_handle* h, u64 entries) {
   Dev& d = h->d;
   u64 cap = pow2_at_least(std::max<u64>(entries, 64));
   if (cap <= d.fcap) return;
+  if (h->dry) {
+    h->dry_hit = true;
+    return;
+  }
   ring_regrow(h, d.fifo_req, d.fcap, cap, h->hot.fifo_head, h->hot.fifo_tail);
   ring_regrow(h, d.fifo_tail, d.fcap, cap, h->hot.fifo_head, h->hot.fifo_tail);
   d.fcap = cap;
@@ -1016,6 +1222,10 @@ void reserve_inflight(e2_handle* h, u64 live) {
   Dev& d = h->d;
   const u64 cap = pow2_at_least(std::max<u64>(4 * live + 64, 1024));
   if (d.inf && cap <= d.inf_mask + 1) return;
+  if (h->dry) {
+    h->dry_hit = true;
+    return;
+  }
   const u64 oc = d.inf ? d.inf_mask + 1 : 0;
   std::vector<InfRec> old(oc);
   if (oc) {
@@ -1042,6 +1252,10 @@ void reserve_inflight(e2_handle* h, u64 live) {
 
 void reserve_tokens(e2_handle* h, i64 need) {
   if (need + 128 <= h->tok_cap) return;
+  if (h->dry) {
+    h->dry_hit = true;
+    return;
+  }
   i64 cap = std::max<i64>(need + 128, h->tok_cap * 2);
   cap = std::max<i64>(cap, 1 << 16);
   grow(h->tok, (size_t)h->tok_len, (size_t)cap, h->stream);
@@ -1059,6 +1273,10 @@ void reserve_requests(e2_handle* h, i64 need) {
 }
 
 void reserve_batch(e2_handle* h, i64 B) {
+  if (h->dry) {
+    if ((h->want_hstride > h->hstride && h->bcap > 0) || B > h->bcap) h->dry_hit = true;
+    return;
+  }
   if (h->want_hstride > h->hstride && h->bcap > 0) {
     // paths got deeper than the hint stride in an earlier batch
     dfree(h->b_path);
@@ -1404,6 +1622,196 @@ void append_host_tokens(e2_handle* h, const i32* seq, i64 len) {
 }
 
 
+// ---- per-call session (host side of k_session) -----------------------------
+e2_handle* g_sess_owner = nullptr;  // at most one session: g_dev is shared by every handle
+bool session_active(const e2_handle* h) { return h->sess_on; }
+
+#if E2_DEVICE_BUILD
+SessCmd* sess_cmd(e2_handle* h) { return (SessCmd*)h->sess_cmd; }
+SessRes* sess_res(e2_handle* h) { return (SessRes*)h->sess_res; }
+
+// Wait until k_session left (stop command, idle timeout or error) and take
+// the state it wrote back to HBM as the device's.
+void session_stop(e2_handle* h) {
+  if (h) h->sess_last_ok = false;
+  if (!h || !h->sess_on) return;
+  h->sess_stops++;
+  SessCmd* c = sess_cmd(h);
+  c->stop = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  c->seq = h->sess_next++;
+  const cudaError_t e = cudaStreamSynchronize(h->sess_stream);
+  c->stop = 0;
+  h->sess_on = false;
+  if (g_sess_owner == h) g_sess_owner = nullptr;
+  if (e != cudaSuccess) throw Fail(E2_ERR_CUDA, std::string("session: ") + cudaGetErrorString(e));
+  h->dev_hot = h->hot;  // the kernel's last published hot state, now in hot_g
+  h->dev_hot_valid = true;
+}
+
+void session_launch(e2_handle* h) {
+  k_session<<<1, 32, h->serial_smem, h->sess_stream>>>(sess_cmd(h), sess_res(h), h->sess_next, h->b_path, h->hstride,
+                                                      h->nsets, h->sess_idle_ns);
+  CK(cudaGetLastError());
+  h->sess_starts++;
+}
+
+void session_start(e2_handle* h) {
+  if (g_sess_owner && g_sess_owner != h) session_stop(g_sess_owner);
+  if (!h->sess_stream) CK(cudaStreamCreateWithFlags(&h->sess_stream, cudaStreamNonBlocking));
+  push_hot(h);
+  upload_dev(h);
+  ssync(h->stream);  // every earlier copy and launch of h is complete
+  memcpy((void*)&sess_res(h)->hot, &h->hot, sizeof(Hot));  // the warp publishes changed words only
+  session_launch(h);
+  h->sess_on = true;
+  g_sess_owner = h;
+}
+
+void session_buffers(e2_handle* h, i64 ntok) {
+  if (h->sess_cmd && ntok <= h->sess_tok_cap) return;
+  session_stop(h);
+  if (h->sess_cmd) cudaFreeHost(h->sess_cmd);
+  h->sess_cmd = nullptr;
+  const i64 cap = std::max<i64>(ntok, std::max<i64>(2 * h->sess_tok_cap, 1 << 14));
+  CK(cudaHostAlloc(&h->sess_cmd, kSessTok + (size_t)cap * 4 + kSessFirst + 64, cudaHostAllocMapped));
+  memset(h->sess_cmd, 0, kSessTok);
+  h->sess_tok_cap = cap;
+  if (!h->sess_res) {
+    CK(cudaHostAlloc(&h->sess_res, sizeof(SessRes), cudaHostAllocMapped));
+    memset(h->sess_res, 0, sizeof(SessRes));
+  }
+  // command numbers restart with the new block (the old one is gone)
+  h->sess_next = 1;
+}
+
+// Would reserve_for / reserve_batch grow anything for this op?
+bool session_fits(e2_handle* h, i64 len, bool need_match) {
+  h->dry = true;
+  h->dry_hit = false;
+  reserve_for(h, 1, len);
+  if (need_match) reserve_batch(h, 1);
+  h->dry = false;
+  return !h->dry_hit;
+}
+
+bool session_kind(i32 k) {
+  switch (k) {
+    case OP_SCHEDULE:
+    case OP_DECIDE:
+    case OP_PREFILL:
+    case OP_EVICT:
+    case OP_FINISHED:
+    case OP_LOAD_COST:
+    case OP_GPU_LOAD:
+    case OP_MATCH:
+    case OP_WINDOW:
+    case OP_INFLIGHT_GET:
+      return true;
+    default:
+      return false;
+  }
+}
+
+// Run one per-call op through the session.  False: not taken (the caller
+// uses the launch path; any running session is stopped first).
+bool session_op(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match, bool transient) {
+  int why = 0;
+  if (h->no_session) why = 1;
+  else if (!session_kind(op.kind)) why = 2;
+  else if (!h->dev_hot_valid || memcmp(&h->hot, &h->dev_hot, sizeof(Hot)) != 0) why = 3;
+  else if (!session_fits(h, seq ? len : 0, need_match)) why = 4;
+  if (why) {
+    h->sess_why[why]++;
+    session_stop(h);
+    return false;
+  }
+  session_buffers(h, seq ? len : 0);
+  if (!h->sess_on) session_start(h);
+  SessCmd* c = sess_cmd(h);
+  SessRes* r = sess_res(h);
+  // the same prompt as the last committed op (schedule, then its
+  // note_prefill_cached): its tokens are already in the arena
+  const bool reuse = seq && h->sess_last_ok && (i64)h->sess_last.size() == len &&
+                     memcmp(h->sess_last.data(), seq, (size_t)len * 4) == 0;
+  if (seq) {
+    if (!reuse) memcpy((char*)c + kSessTok, seq, (size_t)len * 4);
+    op.off = reuse ? h->sess_last_off : h->tok_len;
+    op.len = len;
+    if (need_match) op.L = kMatchInline;
+  }
+  c->op = op;
+  c->ntok = (seq && !reuse) ? len : 0;
+  c->need_match = (seq && need_match) ? 1 : 0;
+  c->stop = 0;
+  const unsigned long long want = h->sess_next;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  c->seq = want;
+  for (u64 spin = 1; r->seq != want; ++spin) {
+    if ((spin & 1023) == 0) {
+      const cudaError_t q = cudaStreamQuery(h->sess_stream);
+      if (q == cudaErrorNotReady) continue;
+      if (q != cudaSuccess) {
+        h->sess_on = false;
+        if (g_sess_owner == h) g_sess_owner = nullptr;
+        throw Fail(E2_ERR_CUDA, std::string("session: ") + cudaGetErrorString(q));
+      }
+      if (r->seq == want) break;
+      // the warp left on its idle timeout before it saw this command: its
+      // hot state is in HBM (h->dev_hot); a fresh warp picks the command up
+      h->sess_relaunch++;
+      session_launch(h);
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  h->sess_next = want + 1;
+  h->sess_ops++;
+  if (seq && !reuse) {
+    if (!transient) {
+      h->sess_last.assign(seq, seq + len);
+      h->sess_last_off = h->tok_len;
+      h->sess_last_ok = true;
+    }
+    h->tok_len += len;
+  }
+  memcpy(&h->hot, (const void*)&r->hot, sizeof(Hot));
+  memcpy(&h->api, (const void*)&r->api, sizeof(ApiOut));
+  h->dev_hot = h->hot;
+  h->dev_hot_valid = true;
+  if (h->hot.err) {
+    session_stop(h);
+    check_hot_error(h);
+  }
+  return true;
+}
+
+void session_free(e2_handle* h) {
+  try {
+    session_stop(h);
+  } catch (...) {
+  }
+  if (h->sess_res && getenv("E2_SESSION_DEBUG")) {
+    const SessRes* r = sess_res(h);
+    const double n = std::max<double>(1.0, (double)r->pad[3]);
+    fprintf(stderr,
+            "session: %lld ops, %lld launches (%lld relaunches), %lld stops, not taken %lld/%lld/%lld/%lld; per op us: "
+            "in %.2f op %.2f out %.2f\n",
+            (long long)h->sess_ops, (long long)h->sess_starts, (long long)h->sess_relaunch, (long long)h->sess_stops,
+            (long long)h->sess_why[1], (long long)h->sess_why[2], (long long)h->sess_why[3], (long long)h->sess_why[4],
+            r->pad[0] / n / 1e3, r->pad[1] / n / 1e3, r->pad[2] / n / 1e3);
+  }
+  if (h->sess_cmd) cudaFreeHost(h->sess_cmd);
+  if (h->sess_res) cudaFreeHost(h->sess_res);
+  if (h->sess_stream) cudaStreamDestroy(h->sess_stream);
+  h->sess_cmd = h->sess_res = nullptr;
+  h->sess_stream = 0;
+}
+#else
+void session_stop(e2_handle*) {}
+bool session_op(e2_handle*, OpDesc, const i32*, i64, bool, bool) { return false; }
+void session_free(e2_handle*) {}
+#endif
+
 // One API op on one sequence (or none): append, match, run.
 // `transient`: the op stores no reference to the sequence (decide, match,
 // note_eviction: splits only cut existing edges), so its arena bytes are
@@ -1418,6 +1826,7 @@ void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match, 
       if (on) h->tok_len = mark;
     }
   } rb{h, tok_mark, transient};
+  if (session_op(h, op, seq, len, need_match, transient)) return;
   reserve_for(h, 1, len);
   if (seq) {
     append_host_tokens(h, seq, len);
@@ -1452,10 +1861,14 @@ void run_api(e2_handle* h, OpDesc op, const i32* seq, i64 len, bool need_match, 
 
 std::recursive_mutex g_lock;  // g_dev (constant memory) is shared by every handle
 
+// guard: every entry point.  Entry points other than the per-call ops
+// (guard_api) first end the running session, so their launches, copies and
+// reads of the HBM hot state see the session's final state.
 template <typename F>
-int guard(e2_handle* h, F&& f) {
+int guard(e2_handle* h, F&& f, bool api = false) {
   std::lock_guard<std::recursive_mutex> lk(g_lock);
   try {
+    if (g_sess_owner && (!api || g_sess_owner != h)) session_stop(g_sess_owner);
     f();
     return E2_OK;
   } catch (const Fail& e) {
@@ -1664,6 +2077,7 @@ void check_autoscale(e2_handle* h, double now) {
       const double pm = pi->second.first / (double)pi->second.second;
       const double cm = ci->second.first / (double)ci->second.second;
       if (pm > 0 && cm >= 2.0 * pm) {
+        session_stop(h);  // host-orchestrated: a tree pull, subtree ops on the launch path
         HostTree t;
         pull_tree(h, t);
         u32 rc = kNil;
@@ -1803,6 +2217,7 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
     }
 #if E2_DEVICE_BUILD
     CK(cudaFuncSetAttribute(k_serial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->serial_smem));
+    CK(cudaFuncSetAttribute(k_session, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->serial_smem));
 #endif
 #if E2_DEVICE_BUILD
     {
@@ -1815,6 +2230,10 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
       h->no_prefetch = npf && npf[0] == '1';
       const char* ntp = getenv("E2_NO_TOP");
       h->no_top = ntp && ntp[0] == '1';
+      const char* nse = getenv("E2_NO_SESSION");
+      h->no_session = nse && nse[0] == '1';
+      const char* sid = getenv("E2_SESSION_IDLE_US");
+      if (sid) h->sess_idle_ns = (u64)std::max(0.0, atof(sid) * 1000.0);
     }
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream_handle = h->stream;
@@ -1859,6 +2278,10 @@ void shadow_free(e2_handle* h);  // (sharded replay, below)
 
 void e2_destroy(e2_handle* h) {
   if (!h) return;
+  {
+    std::lock_guard<std::recursive_mutex> lk(g_lock);
+    session_free(h);
+  }
   shadow_free(h);
   Dev& d = h->d;
   void* ptrs[] = {d.rec, d.ct, d.win, d.comp, d.plog, d.dir, d.pg_la, d.pg_id, d.pg_slot, d.free_pages, d.inf, d.fifo_req,
@@ -1954,7 +2377,7 @@ int e2_schedule(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t
     run_api(h, op, prompt_len ? prompt : &dummy, prompt_len, true);
     copy_decision(h, out, costs, ratios);
     if (h->pol.mode == E2_MODE_PREFIX_AWARE && h->pol.autoscale) check_autoscale(h, now);
-  });
+  }, true);
 }
 
 int e2_decide(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t request_id, double now,
@@ -1968,7 +2391,7 @@ int e2_decide(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int64_t r
     static const i32 dummy = 0;
     run_api(h, op, prompt_len ? prompt : &dummy, prompt_len, true, true);
     copy_decision(h, out, costs, ratios);
-  });
+  }, true);
 }
 
 int e2_note_admitted(e2_handle* h, int64_t request_id, double now) {
@@ -1985,7 +2408,7 @@ int e2_note_admitted(e2_handle* h, int64_t request_id, double now) {
     auto& cell = h->queue_stats[h->api.u0][bucket];
     cell.first += now - h->api.v;
     cell.second += 1;
-  });
+  }, true);
 }
 
 int e2_note_prefill_cached(e2_handle* h, const int32_t* prompt, int64_t prompt_len, int32_t gpu, double now) {
@@ -1998,7 +2421,7 @@ int e2_note_prefill_cached(e2_handle* h, const int32_t* prompt, int64_t prompt_l
     op.gpu = gpu;
     op.now = now;
     run_api(h, op, prompt, prompt_len, true);
-  });
+  }, true);
 }
 
 int e2_note_eviction(e2_handle* h, const int32_t* seq, int64_t seq_len, int64_t tail_len, int32_t gpu, double now) {
@@ -2012,7 +2435,7 @@ int e2_note_eviction(e2_handle* h, const int32_t* seq, int64_t seq_len, int64_t 
     op.x = tail_len;
     op.now = now;
     run_api(h, op, seq, seq_len, true, true);
-  });
+  }, true);
 }
 
 int e2_note_finished(e2_handle* h, int64_t request_id, double now, int64_t output_len) {
@@ -2025,7 +2448,7 @@ int e2_note_finished(e2_handle* h, int64_t request_id, double now, int64_t outpu
     op.now = now;
     op.x = output_len;
     run_api(h, op, nullptr, 0, false);
-  });
+  }, true);
 }
 
 int e2_decode_ratio(e2_handle* h, int32_t gpu, double* out) {
@@ -2034,12 +2457,12 @@ int e2_decode_ratio(e2_handle* h, int32_t gpu, double* out) {
     pull_hot(h);
     const i64 ip = h->hot.inflight_prompt[gpu];
     *out = ip <= 0 ? 0.0 : (double)h->hot.inflight_cached[gpu] / (double)ip;
-  });
+  }, true);
 }
 
 int e2_gpu_load_ms(e2_handle* h, int32_t gpu, double now, double* out) {
   if (bad_gpu(h, gpu)) return E2_ERR_ARG;
-  return guard(h, [&] { *out = host_load(h, gpu, now); });
+  return guard(h, [&] { *out = host_load(h, gpu, now); }, true);
 }
 
 int e2_prune_dead_nodes(e2_handle* h, double now, int64_t* removed) {
@@ -2058,21 +2481,21 @@ int e2_cached_tokens(e2_handle* h, int32_t gpu, int64_t* out) {
   return guard(h, [&] {
     pull_hot(h);
     *out = h->hot.cached_tokens[gpu];
-  });
+  }, true);
 }
 
 int e2_node_count(e2_handle* h, int64_t* out) {
   return guard(h, [&] {
     pull_hot(h);
     *out = h->hot.node_count;
-  });
+  }, true);
 }
 
 int e2_redirects(e2_handle* h, int32_t* out) {
   return guard(h, [&] {
     pull_hot(h);
     for (int g = 0; g < h->G; ++g) out[g] = h->hot.redirect[g];
-  });
+  }, true);
 }
 
 int e2_get_stats(e2_handle* h, e2_stats* out) {
@@ -2086,7 +2509,7 @@ int e2_get_stats(e2_handle* h, e2_stats* out) {
     out->rebalance_installs = h->hot.stats[kStInstalls];
     out->autoscale_events = h->hot.stats[kStAutoscale];
     out->tree_reads = h->hot.stats[kStTreeReads];
-  });
+  }, true);
 }
 
 int e2_load_cost(e2_handle* h, int32_t gpu, int64_t missed_tokens, double now, e2_cost* out) {
@@ -2100,7 +2523,7 @@ int e2_load_cost(e2_handle* h, int32_t gpu, int64_t missed_tokens, double now, e
     op.now = now;
     run_api(h, op, nullptr, 0, false);
     *out = h->api.costs[0];
-  });
+  }, true);
 }
 
 int e2_match(e2_handle* h, const int32_t* seq, int64_t len, int64_t* matched_len, int64_t* cached_len,
@@ -2115,7 +2538,7 @@ int e2_match(e2_handle* h, const int32_t* seq, int64_t len, int64_t* matched_len
     if (cached_len) *cached_len = h->api.i1;
     if (per_gpu)
       for (int g = 0; g < h->G; ++g) per_gpu[g] = h->api.ext[g];
-  });
+  }, true);
 }
 
 int e2_window_sizes(e2_handle* h, int32_t gpu, double now, int64_t* n_scheduled, int64_t* n_completed,
@@ -2132,7 +2555,7 @@ int e2_window_sizes(e2_handle* h, int32_t gpu, double now, int64_t* n_scheduled,
     if (n_completed) *n_completed = h->api.i1;
     if (inflight_cached) *inflight_cached = h->api.i2;
     if (inflight_prompt) *inflight_prompt = h->api.i3;
-  });
+  }, true);
 }
 
 // ---- export / dump (host-side; off the hot path) ---------------------------

@@ -25,3 +25,4 @@ dt = time.perf_counter() - t0
 p = abi.ProfileC(); lib.e2_profile_get(s._h, ctypes.byref(p))
 print(f"{calls} calls in {dt:.3f} s: {1e6 * dt / calls:.1f} us/call wall; serial kernel {1e3 * p.ms[3] / max(1, p.launches[3]):.1f} us/launch "
       f"({p.launches[3]} launches, {100 * p.ms[3] / 1e3 / dt:.0f}% of wall)")
+s.close()

@@ -43,6 +43,7 @@ def _same_decision(a, b):
 
 def run_case(lib, ref_lib, seed, stats):
     rng = random.Random(seed)
+    snap = hasattr(lib, "e2_export_hit_stamps")  # the plain-C oracle has no snapshot()
     n = 2 + rng.randrange(3)
     cfg = SchedulerConfig(
         history_window_ms=rng.choice([600.0, 3000.0, 20000.0]),
@@ -73,7 +74,7 @@ def run_case(lib, ref_lib, seed, stats):
                     extra = 1 + rng.randrange(15)
                     prompt += list(range(unique, unique + extra))
                     unique += extra
-            if rng.randrange(4) == 0:  # the reference harness snapshots before each decision (:333)
+            if snap and rng.randrange(4) == 0:  # the reference harness snapshots before each decision (:333)
                 stats["snapshots"] += 1
                 msg = snapshot_diff(A, B, t)
                 assert msg is None, (seed, op, msg)
@@ -143,8 +144,9 @@ def run_case(lib, ref_lib, seed, stats):
     assert A.redirects() == B.redirects()
     msg = export_diff(A, B, t)
     assert msg is None, (seed, msg)
-    msg = snapshot_diff(A, B, t)
-    assert msg is None, (seed, msg)
+    if snap:
+        msg = snapshot_diff(A, B, t)
+        assert msg is None, (seed, msg)
     A.close()
     B.close()
 
