@@ -837,10 +837,22 @@ E2_DNI Walk walk_par(const i32* seq, i64 L, const u32* hint, int nhint, Scr* s, 
 // Warp-wide.
 // The LRU re-indexing of the path, after path_update_par (deferred variant:
 // run by the eviction warp of the pipelined replay before its eviction).
+E2_DNI void fix_level(const Scr* s, int i, int g);
 E2_DNI void path_lru_fix(const Scr* s, int D, int g) {
-  for (int i = 0; i < D; ++i) {
+  // the flagged levels (usually the last one or two) found kWidth at a time
+  for (int b = 0; b < D; b += kWidth) {
+    u32 m = ballot(b + lane() < D && (PFLAG(s, b + lane()) & 8u));
+    while (m) {
+      const int i = b + ffs32(m);
+      m &= m - 1;
+      fix_level(s, i, g);
+    }
+  }
+}
+
+E2_DNI void fix_level(const Scr* s, int i, int g) {
+  {
     const u32 f = PFLAG(s, i);
-    if (!(f & 8u)) continue;
     const u32 v = PSLOT(s, i);
     const NodeRec* r = nget(v);
     const u64 id = r->id, la1 = dbits(rla(r)[g]);
@@ -850,6 +862,22 @@ E2_DNI void path_lru_fix(const Scr* s, int D, int g) {
 }
 
 // defer: leave the LRU re-indexing to path_lru_fix (s->fix_D = D).
+#if E2_WARP
+#ifndef E2_PF_CHUNKS
+#define E2_PF_CHUNKS 3
+#endif
+constexpr int kPfChunks = E2_PF_CHUNKS;
+// the lines of a path record the path update reads and writes on g
+E2_D void pf_path_rec(u32 v, int g, int G) {
+  if (v >= DEV.node_cap) return;
+  const char* r = (const char*)grec(v);
+  pf(r);
+  pf(r + 64 + 8 * g);
+  pf(r + 64 + 8 * G + 4 * g);
+  pf(r + 64 + 12 * G + 4 * g);
+}
+#endif
+
 E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark, bool defer = false) {
   const int G = DEV.cfg.G;
   // the parent's cached-child count uses its child's "newly cached" flag:
@@ -857,7 +885,15 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark, bool def
   // the path fits a warp, else from a first pass through shared memory
   const bool onepass = E2_WARP && D <= kWidth;
   if (!onepass) {
+#if E2_WARP
+    // deep paths: the first kPfChunks chunks' record lines in flight at once,
+    // then each chunk prefetches the one kPfChunks ahead
+    for (int i = lane(); i < D && i < kPfChunks * kWidth; i += kWidth) pf_path_rec(PSLOT(s, i), g, G);
+#endif
     for (int i = lane(); i < D; i += kWidth) {
+#if E2_WARP
+      if (i + kPfChunks * kWidth < D) pf_path_rec(PSLOT(s, i + kPfChunks * kWidth), g, G);
+#endif
       const NodeRec* r = npeek(PSLOT(s, i));
       PFLAG(s, i) = (mark && !rcached(r, g)) ? 1u : 0u;
     }
@@ -866,9 +902,16 @@ E2_DNI u64 path_update_par(Scr* s, int D, int g, double now, bool mark, bool def
   i64 add = 0;
   u32 any = 0;
   u64 id0 = 0;
+#if E2_WARP
+  if (!onepass)
+    for (int i = lane(); i < D && i < kPfChunks * kWidth; i += kWidth) pf_path_rec(PSLOT(s, i), g, G);
+#endif
   for (int b = 0; b < D; b += kWidth) {
     const int i = b + lane();
     const bool in = i < D;
+#if E2_WARP
+    if (!onepass && i + kPfChunks * kWidth < D) pf_path_rec(PSLOT(s, i + kPfChunks * kWidth), g, G);
+#endif
     NodeRec* r = in ? npoke(PSLOT(s, i)) : nullptr;
     const bool was = in && rcached(r, g);
     bool newly, inc;
