@@ -2218,6 +2218,13 @@ int e2_create(int32_t n_gpus, const e2_sched_cfg* cfg, const e2_time_model* mode
 #if E2_DEVICE_BUILD
     CK(cudaFuncSetAttribute(k_serial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->serial_smem));
     CK(cudaFuncSetAttribute(k_session, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->serial_smem));
+#if !defined(E2_NO_L1_PREF)
+    // the serial kernel is one block per SM: the smallest shared-memory
+    // configuration that fits it leaves the rest to L1 (A/B: C4 +4.5 %,
+    // C2 +2.3 %, C5 +3.8 % together with the 512-level path scratch)
+    CK(cudaFuncSetAttribute(k_serial, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_session, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+#endif
 #endif
 #if E2_DEVICE_BUILD
     {

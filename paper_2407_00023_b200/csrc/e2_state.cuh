@@ -104,7 +104,10 @@ constexpr i64 kNoInflight = INT64_MIN;
 constexpr int kPage = 32;   // LRU keys per page
 constexpr int kPathHint = 1024;  // initial K1 hint stride (path slots per request, kNil-terminated)
 constexpr int kMaxHint = 16384;  // largest hint stride the host grows to
-constexpr int kMaxPath = 1024;  // path levels a request keeps in shared memory
+#ifndef E2_MAX_PATH
+#define E2_MAX_PATH 512  // 1024 measured slower: the larger scratch takes shared memory from L1
+#endif
+constexpr int kMaxPath = E2_MAX_PATH;  // path levels a request keeps in shared memory
 constexpr u32 kXPath = 1u << 16;  // deeper levels: global overflow (DEV.xp_*)
 
 // Error codes mirrored from e2sched.h.

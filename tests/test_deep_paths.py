@@ -1,5 +1,5 @@
 """Deep radix paths: a chain whose every request extends the previous one,
-so request i's path has i levels.  Past 1024 levels the engine keeps path
+so request i's path has i levels.  Past kMaxPath (512) levels the engine keeps path
 levels in its global overflow arrays, K1 grows its hint stride between
 batches, and hit stamps are undone through the path log — all of it must
 still match the reference bit for bit (decisions, costs, final mirror).
@@ -59,7 +59,7 @@ def _check(lib, ref_lib, n, cap, hw, batch):
 
 
 def test_deep_chain_hostsim(hostsim_lib, ref_lib):
-    # 1400 requests: the chain path reaches ~1120 levels (> kMaxPath = 1024);
+    # 1400 requests: the chain path reaches ~1120 levels (> kMaxPath = 512);
     # the tight capacity makes the eviction term and hit catch-up run on it
     _check(hostsim_lib, ref_lib, 1400, 20000, 16000, 256)
 
